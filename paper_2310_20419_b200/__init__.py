@@ -1,0 +1,8 @@
+"""B200-native RNN-Descent graph builder (arXiv 2310.20419 hot path).
+
+The product is librnndg.so (sm_100a CUDA kernels + host orchestration behind
+the C ABI in include/rnndg.h).  `rnnd` mirrors the reference C++ API on top of
+it; `datagen` exposes the seeded BASELINE.json input generators.
+"""
+from . import rnnd  # noqa: F401
+from .rnnd import *  # noqa: F401,F403

@@ -1,0 +1,105 @@
+"""ctypes binding of librnndg.so (include/rnndg.h).
+
+There is no fallback: if the CUDA library is missing this module raises, and
+every compute entry point needs a visible GPU.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "librnndg.so")
+
+OK, EPARAM, EDATA, EINTERNAL = 0, 1, 2, 3
+
+u8p = C.POINTER(C.c_uint8)
+u32p = C.POINTER(C.c_uint32)
+u64p = C.POINTER(C.c_uint64)
+f32p = C.POINTER(C.c_float)
+
+
+class Counts(C.Structure):
+    """rnndg_counts == rnnd::EditCounts (builder.hpp:25-38)."""
+
+    _fields_ = [("removed", C.c_uint64), ("inserted", C.c_uint64),
+                ("flag_skips", C.c_uint64), ("pair_checks", C.c_uint64)]
+
+
+class BuildStatsC(C.Structure):
+    _fields_ = [("seconds", C.c_double), ("update_passes", C.c_uint32),
+                ("reverse_phases", C.c_uint32), ("edits", Counts),
+                ("scan_seconds", C.c_double), ("sort_seconds", C.c_double),
+                ("apply_seconds", C.c_double), ("reverse_seconds", C.c_double),
+                ("touched", C.c_uint64), ("active_entries", C.c_uint64),
+                ("scan_launches", C.c_uint64), ("kernel_launches", C.c_uint64)]
+
+
+PROGRESS_FN = C.CFUNCTYPE(None, C.c_uint32, C.c_uint32, C.POINTER(Counts), C.c_double,
+                          C.c_void_p)
+
+_LIB = None
+
+
+def lib() -> C.CDLL:
+    """Load librnndg.so, raising loudly when the CUDA extension is absent."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(
+            f"{LIB_PATH} is missing: the CUDA extension is not built "
+            "(run `python -c 'import __graft_entry__ as g; g.build()'`)")
+    L = C.CDLL(LIB_PATH)
+    vp = C.c_void_p
+    sig = {
+        "rnndg_create": (C.c_int, [C.POINTER(vp), C.c_int]),
+        "rnndg_destroy": (C.c_int, [vp]),
+        "rnndg_last_error": (C.c_char_p, [vp]),
+        "rnndg_kernel_launches": (C.c_uint64, [vp]),
+        "rnndg_set_data": (C.c_int, [vp, f32p, C.c_uint64, C.c_uint32]),
+        "rnndg_set_data_device": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32]),
+        "rnndg_random_init": (C.c_int, [vp, C.c_uint32, C.c_uint64]),
+        "rnndg_update_pass": (C.c_int, [vp, C.POINTER(Counts)]),
+        "rnndg_reverse": (C.c_int, [vp, C.c_uint32, C.c_int]),
+        "rnndg_sort_lists": (C.c_int, [vp]),
+        "rnndg_build": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                  C.c_uint64, C.c_int, C.POINTER(BuildStatsC),
+                                  PROGRESS_FN, vp]),
+        "rnndg_pass_counts": (C.c_int, [vp, C.POINTER(Counts), C.c_uint32]),
+        "rnndg_graph_size": (C.c_int, [vp, u64p, u64p]),
+        "rnndg_get_graph": (C.c_int, [vp, u64p, u32p, f32p, u8p]),
+        "rnndg_set_graph": (C.c_int, [vp, C.c_uint64, u64p, u32p, f32p, u8p]),
+        "rnndg_index_bytes": (C.c_int, [vp, u8p, u64p]),
+        "rnndg_degree_stats": (C.c_int, [vp, C.c_uint32, u64p]),
+        "rnndg_search": (C.c_int, [vp, f32p, C.c_uint64, C.c_uint32, C.c_uint32,
+                                   C.c_uint32, C.c_int, C.c_uint32, C.c_uint32,
+                                   C.c_uint64, u32p, f32p, u64p, u64p]),
+        "rnndg_brute_force": (C.c_int, [vp, f32p, C.c_uint64, C.c_uint32, u32p]),
+        "rnndg_rng_strategy": (C.c_int, [vp, C.c_uint32, u32p, f32p, C.c_uint32, u32p,
+                                         f32p, u32p]),
+        "rnndg_l2_pairs": (C.c_int, [vp, u32p, u32p, C.c_uint64, f32p]),
+        "rnndg_synth_dim": (C.c_uint32, [C.c_int]),
+        "rnndg_synth": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, f32p]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(L, name)
+        fn.restype = res
+        fn.argtypes = args
+    _LIB = L
+    return L
+
+
+def ptr(a, t):
+    return a.ctypes.data_as(t)
+
+
+# every symbol include/rnndg.h declares (checked by tests/test_abi.py)
+EXPORTED = (
+    "rnndg_create", "rnndg_destroy", "rnndg_last_error", "rnndg_kernel_launches",
+    "rnndg_set_data", "rnndg_set_data_device", "rnndg_random_init",
+    "rnndg_update_pass", "rnndg_reverse", "rnndg_sort_lists", "rnndg_build",
+    "rnndg_pass_counts", "rnndg_graph_size", "rnndg_get_graph", "rnndg_set_graph",
+    "rnndg_index_bytes", "rnndg_degree_stats", "rnndg_search", "rnndg_brute_force",
+    "rnndg_rng_strategy", "rnndg_l2_pairs", "rnndg_synth_dim", "rnndg_synth",
+)

@@ -1,0 +1,415 @@
+// api.cu -- the extern "C" boundary (include/rnndg.h).  Each entry point
+// validates like the reference function it replaces, maps exceptions to the
+// reference's error classes, and runs the work on the context's device.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "ctx.hpp"
+
+using namespace rnndg;
+
+namespace {
+
+template <class Fn>
+int guarded(rnndg_ctx* c, Fn fn) {
+  if (!c) return RNNDG_EPARAM;
+  try {
+    RNNDG_CUDA(cudaSetDevice(c->device));
+    fn();
+    c->err.clear();
+    return RNNDG_OK;
+  } catch (const rnndg::ParamError& e) {
+    c->err = e.what();
+    return RNNDG_EPARAM;
+  } catch (const rnndg::DataError& e) {
+    c->err = e.what();
+    return RNNDG_EDATA;
+  } catch (const std::exception& e) {
+    c->err = e.what();
+    return RNNDG_EINTERNAL;
+  }
+}
+
+void need_data(rnndg_ctx* c) {
+  if (!c->x || c->n == 0) throw ParamError("no vector data: call rnndg_set_data first");
+}
+void need_graph(rnndg_ctx* c) {
+  need_data(c);
+  if (!c->has_graph) throw ParamError("no graph on the context");
+}
+
+// zlib crc32 (graph.cpp:41-43): IEEE 802.3, reflected polynomial 0xEDB88320
+uint32_t crc32_ieee(const uint8_t* p, size_t size) {
+  static uint32_t table[256];
+  static bool init = false;
+  if (!init) {
+    for (uint32_t i = 0; i < 256; ++i) {
+      uint32_t c = i;
+      for (int k = 0; k < 8; ++k) c = (c & 1) ? 0xEDB88320u ^ (c >> 1) : c >> 1;
+      table[i] = c;
+    }
+    init = true;
+  }
+  uint32_t c = 0xFFFFFFFFu;
+  for (size_t i = 0; i < size; ++i) c = table[(c ^ p[i]) & 0xFF] ^ (c >> 8);
+  return c ^ 0xFFFFFFFFu;
+}
+
+// device CSR (capacity layout) -> host (counts, keys) in list order
+void fetch_graph(rnndg_ctx* c, std::vector<uint64_t>& off, std::vector<uint32_t>& cnt,
+                 std::vector<uint64_t>& keys) {
+  const uint64_t n = c->n;
+  off.resize(n + 1);
+  cnt.resize(n);
+  RNNDG_CUDA(cudaMemcpyAsync(off.data(), c->off.p, (n + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaMemcpyAsync(cnt.data(), c->cnt.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+  keys.resize(c->span ? c->span : 1);
+  if (c->span)
+    RNNDG_CUDA(cudaMemcpyAsync(keys.data(), c->key.p, c->span * 8, cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+float bits_to_float(uint32_t b) {
+  float f;
+  std::memcpy(&f, &b, 4);
+  return f;
+}
+
+}  // namespace
+
+extern "C" {
+
+int rnndg_create(rnndg_ctx** out, int device) {
+  if (!out) return RNNDG_EPARAM;
+  *out = nullptr;
+  auto* c = new rnndg_ctx;
+  c->device = device;
+  try {
+    int ndev = 0;
+    RNNDG_CUDA(cudaGetDeviceCount(&ndev));
+    if (device < 0 || device >= ndev) throw ParamError("rnndg_create: no such device");
+    RNNDG_CUDA(cudaSetDevice(device));
+    RNNDG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    for (auto& e : c->ev) RNNDG_CUDA(cudaEventCreate(&e));
+  } catch (const ParamError&) {
+    delete c;
+    return RNNDG_EPARAM;
+  } catch (...) {
+    delete c;
+    return RNNDG_EINTERNAL;
+  }
+  *out = c;
+  return RNNDG_OK;
+}
+
+int rnndg_destroy(rnndg_ctx* c) {
+  if (!c) return RNNDG_OK;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return RNNDG_OK;
+}
+
+const char* rnndg_last_error(const rnndg_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+uint64_t rnndg_kernel_launches(const rnndg_ctx* c) { return c ? c->launches : 0; }
+
+int rnndg_set_data(rnndg_ctx* c, const float* rows, uint64_t n, uint32_t d) {
+  return guarded(c, [&] {
+    if (!rows || n == 0 || d == 0) throw ParamError("set_data: empty store");
+    if (n >= (1ull << 31)) throw ParamError("set_data: n must be < 2^31");
+    c->x_own.ensure(n * d);
+    RNNDG_CUDA(cudaMemcpyAsync(c->x_own.p, rows, n * d * 4, cudaMemcpyHostToDevice, c->stream));
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+    c->x = c->x_own.p;
+    c->n = n;
+    c->d = d;
+    c->has_graph = false;
+  });
+}
+
+int rnndg_set_data_device(rnndg_ctx* c, const float* rows_dev, uint64_t n, uint32_t d) {
+  return guarded(c, [&] {
+    if (!rows_dev || n == 0 || d == 0) throw ParamError("set_data: empty store");
+    if (n >= (1ull << 31)) throw ParamError("set_data: n must be < 2^31");
+    if (d % 4 == 0 && (reinterpret_cast<uintptr_t>(rows_dev) & 15))
+      throw ParamError("set_data_device: rows must be 16-byte aligned");
+    c->x_own.release();
+    c->x = rows_dev;
+    c->n = n;
+    c->d = d;
+    c->has_graph = false;
+  });
+}
+
+int rnndg_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
+  return guarded(c, [&] {
+    need_data(c);
+    op_random_init(c, S, seed);
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int rnndg_update_pass(rnndg_ctx* c, rnndg_counts* out) {
+  return guarded(c, [&] {
+    need_graph(c);
+    if (!c->has_distances) throw ParamError("update_neighbors: graph has no distances");
+    rnndg_counts cc{};
+    op_update_pass(c, &cc, nullptr, nullptr, nullptr, nullptr, nullptr);
+    if (out) *out = cc;
+  });
+}
+
+int rnndg_reverse(rnndg_ctx* c, uint32_t R, int order) {
+  return guarded(c, [&] {
+    need_graph(c);
+    op_reverse(c, R, order);
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int rnndg_sort_lists(rnndg_ctx* c) {
+  return guarded(c, [&] {
+    need_graph(c);
+    op_sort_lists(c);
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int rnndg_build(rnndg_ctx* c, uint32_t S, uint32_t R, uint32_t T1, uint32_t T2,
+                uint64_t seed, int order, rnndg_build_stats* stats,
+                rnndg_progress_fn progress, void* user) {
+  return guarded(c, [&] {
+    need_data(c);
+    // builder.cpp:255-258
+    if (c->n < 2) throw ParamError("build: need at least 2 vectors");
+    if (S < 1 || S > c->n - 1) throw ParamError("build: S out of [1, n-1]");
+    if (R < 1) throw ParamError("build: R must be >= 1");
+    if (T1 < 1 || T2 < 1) throw ParamError("build: T1 and T2 must be >= 1");
+    rnndg_build_stats st{};
+    const uint64_t launches0 = c->launches;
+    c->pass_counts.clear();
+    RNNDG_CUDA(cudaEventRecord(c->ev[4], c->stream));
+    op_random_init(c, S, seed);
+    for (uint32_t t1 = 1; t1 <= T1; ++t1) {
+      rnndg_counts outer{};
+      for (uint32_t t2 = 0; t2 < T2; ++t2) {
+        rnndg_counts pc{};
+        op_update_pass(c, &pc, &st.scan_seconds, &st.sort_seconds, &st.apply_seconds,
+                       &st.touched, &st.active_entries);
+        c->pass_counts.push_back(pc);
+        outer.removed += pc.removed;
+        outer.inserted += pc.inserted;
+        outer.flag_skips += pc.flag_skips;
+        outer.pair_checks += pc.pair_checks;
+        ++st.update_passes;
+      }
+      if (t1 != T1) {
+        RNNDG_CUDA(cudaEventRecord(c->ev[6], c->stream));
+        op_reverse(c, R, order);
+        RNNDG_CUDA(cudaEventRecord(c->ev[7], c->stream));
+        RNNDG_CUDA(cudaEventSynchronize(c->ev[7]));
+        float ms = 0.f;
+        RNNDG_CUDA(cudaEventElapsedTime(&ms, c->ev[6], c->ev[7]));
+        st.reverse_seconds += ms * 1e-3;
+        ++st.reverse_phases;
+      }
+      st.edits.removed += outer.removed;
+      st.edits.inserted += outer.inserted;
+      st.edits.flag_skips += outer.flag_skips;
+      st.edits.pair_checks += outer.pair_checks;
+      if (progress) {
+        RNNDG_CUDA(cudaEventRecord(c->ev[5], c->stream));
+        RNNDG_CUDA(cudaEventSynchronize(c->ev[5]));
+        float ms = 0.f;
+        RNNDG_CUDA(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]));
+        progress(t1, T1, &outer, ms * 1e-3, user);
+      }
+    }
+    op_sort_lists(c);  // builder.cpp:283-285
+    RNNDG_CUDA(cudaEventRecord(c->ev[5], c->stream));
+    RNNDG_CUDA(cudaEventSynchronize(c->ev[5]));
+    float ms = 0.f;
+    RNNDG_CUDA(cudaEventElapsedTime(&ms, c->ev[4], c->ev[5]));
+    st.seconds = ms * 1e-3;
+    st.kernel_launches = c->launches - launches0;
+    st.scan_launches = st.update_passes;
+    if (stats) *stats = st;
+  });
+}
+
+int rnndg_pass_counts(const rnndg_ctx* c, rnndg_counts* out, uint32_t cap) {
+  if (!c) return RNNDG_EPARAM;
+  const uint32_t m = uint32_t(std::min<size_t>(cap, c->pass_counts.size()));
+  for (uint32_t i = 0; i < m; ++i) out[i] = c->pass_counts[i];
+  return RNNDG_OK;
+}
+
+int rnndg_graph_size(rnndg_ctx* c, uint64_t* n, uint64_t* edges) {
+  return guarded(c, [&] {
+    need_graph(c);
+    std::vector<uint32_t> cnt(c->n);
+    RNNDG_CUDA(cudaMemcpyAsync(cnt.data(), c->cnt.p, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+    uint64_t m = 0;
+    for (uint32_t v : cnt) m += v;
+    if (n) *n = c->n;
+    if (edges) *edges = m;
+  });
+}
+
+int rnndg_get_graph(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,
+                    uint8_t* fresh) {
+  return guarded(c, [&] {
+    need_graph(c);
+    std::vector<uint64_t> off, keys;
+    std::vector<uint32_t> cnt;
+    fetch_graph(c, off, cnt, keys);
+    uint64_t w = 0;
+    for (uint64_t u = 0; u < c->n; ++u) {
+      if (offsets) offsets[u] = w;
+      for (uint32_t j = 0; j < cnt[u]; ++j, ++w) {
+        const uint64_t k = keys[off[u] + j];
+        if (ids) ids[w] = key_id(k);
+        if (dists) dists[w] = bits_to_float(key_dbits(k));
+        if (fresh) fresh[w] = uint8_t(key_fresh(k));
+      }
+    }
+    if (offsets) offsets[c->n] = w;
+  });
+}
+
+int rnndg_set_graph(rnndg_ctx* c, uint64_t n, const uint64_t* offsets, const uint32_t* ids,
+                    const float* dists, const uint8_t* fresh) {
+  return guarded(c, [&] {
+    need_data(c);
+    if (n != c->n) throw DataError("set_graph: graph size does not match the store");
+    if (!offsets) throw ParamError("set_graph: offsets required");
+    if (offsets[0] != 0) throw DataError("set_graph: bad offsets");
+    for (uint64_t u = 0; u < n; ++u)
+      if (offsets[u + 1] < offsets[u]) throw DataError("set_graph: bad offsets");
+    const uint64_t m = offsets[n];
+    if (m && !ids) throw ParamError("set_graph: ids required");
+    std::vector<uint64_t> keys(m ? m : 1);
+    std::vector<uint32_t> cnt(n);
+    std::vector<uint32_t> scratch;
+    for (uint64_t u = 0; u < n; ++u) {
+      const uint64_t a = offsets[u], b = offsets[u + 1];
+      if (b - a >= (1ull << 32)) throw DataError("set_graph: list too long");
+      cnt[u] = uint32_t(b - a);
+      scratch.assign(ids + a, ids + b);
+      for (uint64_t j = a; j < b; ++j) {
+        if (ids[j] >= n) throw DataError("set_graph: id out of range");
+        if (ids[j] == u) throw DataError("set_graph: self-loop");
+        float dv = dists ? dists[j] : 0.0f;
+        if (dists && !(dv >= 0.0f)) throw DataError("set_graph: distance must be >= 0");
+        if (dv == 0.0f) dv = 0.0f;  // canonical +0
+        keys[j] = make_key(dv, ids[j], fresh ? (fresh[j] ? 1u : 0u) : 0u);
+      }
+      std::sort(scratch.begin(), scratch.end());
+      if (std::adjacent_find(scratch.begin(), scratch.end()) != scratch.end())
+        throw DataError("set_graph: duplicate edge");
+    }
+    c->off.ensure(n + 1);
+    c->cnt.ensure(n + 1);
+    c->key.ensure(m ? m : 1);
+    RNNDG_CUDA(cudaMemcpyAsync(c->off.p, offsets, (n + 1) * 8, cudaMemcpyHostToDevice, c->stream));
+    RNNDG_CUDA(cudaMemcpyAsync(c->cnt.p, cnt.data(), n * 4, cudaMemcpyHostToDevice, c->stream));
+    if (m) RNNDG_CUDA(cudaMemcpyAsync(c->key.p, keys.data(), m * 8, cudaMemcpyHostToDevice, c->stream));
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+    c->span = m;
+    c->has_graph = true;
+    c->has_distances = dists != nullptr;
+  });
+}
+
+int rnndg_index_bytes(rnndg_ctx* c, uint8_t* buf, uint64_t* size) {
+  return guarded(c, [&] {
+    need_graph(c);
+    std::vector<uint64_t> off, keys;
+    std::vector<uint32_t> cnt;
+    fetch_graph(c, off, cnt, keys);
+    uint64_t m = 0;
+    for (uint32_t v : cnt) m += v;
+    const uint64_t total = 16 + (c->n + 1) * 8 + m * 4 + 4;
+    if (size) *size = total;
+    if (!buf) return;
+    // graph.cpp:102-126: "RNND", u32 version 1, u64 n, u64 offsets[n+1],
+    // u32 ids, u32 CRC-32 of everything before; little-endian
+    uint8_t* p = buf;
+    auto put32 = [&](uint32_t v) {
+      for (int i = 0; i < 4; ++i) *p++ = uint8_t(v >> (8 * i));
+    };
+    auto put64 = [&](uint64_t v) {
+      put32(uint32_t(v));
+      put32(uint32_t(v >> 32));
+    };
+    std::memcpy(p, "RNND", 4);
+    p += 4;
+    put32(1);
+    put64(c->n);
+    uint64_t o = 0;
+    put64(o);
+    for (uint64_t u = 0; u < c->n; ++u) {
+      o += cnt[u];
+      put64(o);
+    }
+    for (uint64_t u = 0; u < c->n; ++u)
+      for (uint32_t j = 0; j < cnt[u]; ++j) put32(key_id(keys[off[u] + j]));
+    put32(crc32_ieee(buf, size_t(p - buf)));
+  });
+}
+
+int rnndg_degree_stats(rnndg_ctx* c, uint32_t cap, uint64_t out[3]) {
+  return guarded(c, [&] {
+    need_graph(c);
+    op_degree_stats(c, cap, out);
+  });
+}
+
+int rnndg_search(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t L, uint32_t K,
+                 uint32_t k, int entry_mode, uint32_t entry_vertex, uint32_t entry_count,
+                 uint64_t seed, uint32_t* ids, float* dists, uint64_t* visited,
+                 uint64_t* dist_comps) {
+  return guarded(c, [&] {
+    need_graph(c);
+    op_search(c, queries, nq, L, K, k, entry_mode, entry_vertex, entry_count, seed, ids,
+              dists, visited, dist_comps);
+  });
+}
+
+int rnndg_brute_force(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t k,
+                      uint32_t* ids) {
+  return guarded(c, [&] {
+    need_data(c);
+    op_brute_force(c, queries, nq, k, ids);
+  });
+}
+
+int rnndg_rng_strategy(rnndg_ctx* c, uint32_t u, const uint32_t* cand_ids,
+                       const float* cand_dists, uint32_t ncand, uint32_t* kept_ids,
+                       float* kept_dists, uint32_t* nkept) {
+  return guarded(c, [&] {
+    need_data(c);
+    const uint32_t m = op_rng_strategy(c, u, cand_ids, cand_dists, ncand, kept_ids, kept_dists);
+    if (nkept) *nkept = m;
+  });
+}
+
+int rnndg_l2_pairs(rnndg_ctx* c, const uint32_t* a, const uint32_t* b, uint64_t npairs,
+                   float* out) {
+  return guarded(c, [&] {
+    need_data(c);
+    for (uint64_t i = 0; i < npairs; ++i)
+      if (a[i] >= c->n || b[i] >= c->n) throw ParamError("l2_pairs: id out of range");
+    op_l2_pairs(c, a, b, npairs, out);
+  });
+}
+
+}  // extern "C"

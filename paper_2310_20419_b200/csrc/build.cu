@@ -1,0 +1,755 @@
+// build.cu -- the RNN-Descent update loop on sm_100a.
+//
+// Reference: /root/reference/proj/src/builder.cpp (update_parallel :88-139,
+// scan_vertex :41-69, add_reverse_edges :222-251, out_prune :141-150,
+// in_prune :152-192, final sort :283-285) and graph.cpp random_init :47-63.
+//
+// State is a set of entries per vertex; every step below is order-canonical
+// (sorted scans, set-union appends, sort-based prunes), so the device graph is
+// identical, entry for entry, to rnnd::build with threads > 1.
+//
+// One update pass (all on one stream, no host round trip except the size of
+// the rebuilt CSR):
+//   k_mark_active    vertices with >= 1 fresh entry; inactive ones are exact
+//                    no-ops contributing U(U-1)/2 flag skips
+//   segmented sort   active lists ascending (dist, id)  (builder.cpp:48)
+//   k_scan           occlusion scan + redirect emission (builder.cpp:50-68)
+//   bucket pending   by redirect source (count fused into k_scan, scan,
+//                    k_scatter)
+//   k_apply_count    dedupe + append-if-absent decisions (builder.cpp:117-136)
+//   scan + k_rebuild new CSR
+#define CCCL_IGNORE_DEPRECATED_API
+#include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
+#include <cub/iterator/transform_input_iterator.cuh>
+
+#include "common.cuh"
+#include "ctx.hpp"
+
+namespace rnndg {
+
+namespace {
+
+constexpr int kWarpsPerBlock = 8;
+constexpr int kBlock = 32 * kWarpsPerBlock;
+
+struct ToU64 {
+  __host__ __device__ uint64_t operator()(uint32_t v) const { return v; }
+};
+
+__device__ __forceinline__ unsigned long long warp_sum(unsigned long long v) {
+#pragma unroll
+  for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ void warp_add_counter(unsigned long long* ctr,
+                                                 unsigned long long v) {
+  v = warp_sum(v);
+  if (lane_id() == 0 && v) atomicAdd(ctr, v);
+}
+
+// ------------------------------------------------------------- random init
+// graph.cpp:47-63.  One warp per vertex: lane 0 runs Floyd's sampling
+// (rng.hpp:46-72; the emitted-set test is a linear scan, which is exactly the
+// reference's S <= 64 branch and equivalent to its hash-set branch), then the
+// warp computes the S cached distances.
+template <bool kVec4>
+__global__ void k_random_init(uint64_t n, uint32_t S, uint64_t seed,
+                              const float* __restrict__ x, uint32_t d,
+                              uint64_t* __restrict__ key) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  for (uint64_t u = warp; u < n; u += nwarps) {
+    uint64_t* out = key + u * S;
+    if (lane == 0) {
+      SplitMix64 rng(mix_seed(seed, u));
+      const uint32_t domain = uint32_t(n - 1);  // exclude u
+      uint32_t m = 0;
+      for (uint32_t j = domain - S; j < domain; ++j) {
+        uint32_t t = uint32_t(rng.bounded(uint64_t(j) + 1));
+        bool hit = false;
+        for (uint32_t q = 0; q < m; ++q)
+          if (uint32_t(out[q]) == t) {
+            hit = true;
+            break;
+          }
+        out[m++] = hit ? j : t;
+      }
+    }
+    __syncwarp();
+    for (uint32_t j = lane; j < S; j += 32) {
+      uint32_t id = uint32_t(out[j]);
+      if (id >= u) ++id;  // shift past the excluded pivot (rng.hpp:68-70)
+      float dist = l2_exact<kVec4>(x + u * d, x + uint64_t(id) * d, d);
+      out[j] = make_key(dist, id, 1u);
+    }
+    __syncwarp();
+  }
+}
+
+__global__ void k_fill_offsets(uint64_t n, uint32_t S, uint64_t* off,
+                               uint32_t* cnt) {
+  uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u <= n) off[u] = u * S;
+  if (u < n) cnt[u] = S;
+}
+
+// ------------------------------------------------------------ mark active
+// A vertex with no fresh entry is an exact no-op of scan_vertex: every pair
+// is old/old, nothing is removed, the list keeps its set of entries
+// (builder.cpp:53-56) and it contributes U(U-1)/2 flag skips.
+__global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
+                              const uint32_t* __restrict__ cnt,
+                              const uint64_t* __restrict__ key,
+                              uint8_t* __restrict__ active,
+                              uint64_t* __restrict__ seg_end,
+                              uint32_t* __restrict__ act_list,
+                              uint32_t* __restrict__ post_cnt,
+                              unsigned long long* __restrict__ ctr) {
+  uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long skips = 0, aentries = 0;
+  bool act = false;
+  if (u < n) {
+    const uint64_t b = off[u];
+    const uint32_t U = cnt[u];
+    for (uint32_t j = 0; j < U; ++j)
+      if (key_fresh(key[b + j])) {
+        act = true;
+        break;
+      }
+    active[u] = act ? 1 : 0;
+    seg_end[u] = act ? b + U : b;
+    if (act) {
+      aentries = U;
+    } else {
+      post_cnt[u] = U;
+      skips = (unsigned long long)U * (U ? U - 1 : 0) / 2;
+    }
+  }
+  // warp-aggregated append of active ids
+  unsigned mask = __ballot_sync(0xffffffffu, act);
+  uint32_t base = 0;
+  if (lane_id() == 0 && mask)
+    base = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kActiveCount]), __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, 0);
+  if (act) act_list[base + __popc(mask & ((1u << lane_id()) - 1))] = uint32_t(u);
+  warp_add_counter(&ctr[kFlagSkips], skips);
+  warp_add_counter(&ctr[kActiveEntries], aentries);
+}
+
+// ------------------------------------------------------------------- scan
+// scan_vertex, builder.cpp:45-69, one warp per active vertex.  The list is
+// already sorted by (dist, id).  Kept entries are compacted in place to the
+// front of the list (kept position <= candidate position), so the kept list
+// K is read back from L1/L2.  For candidate v the warp evaluates up to 32
+// kept entries at once (one lane per pair, exact L2) and takes the FIRST
+// occluder in K order via ballot, which reproduces the reference's early
+// break and its exact pair_checks / flag_skips counts.
+//
+// A removed candidate at sorted slot s emits the redirect (w, v, d(v,w)) into
+// pend_src/pend_key[s] and bumps the bucket count of w.
+template <bool kVec4>
+__global__ void __launch_bounds__(kBlock)
+    k_scan(const uint32_t* __restrict__ act_list,
+           const unsigned long long* ctr_in,
+           const uint64_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+           uint64_t* __restrict__ keys, const float* __restrict__ x,
+           uint32_t d, uint32_t* __restrict__ post_cnt,
+           uint32_t* __restrict__ pend_src, uint64_t* __restrict__ pend_key,
+           unsigned long long* __restrict__ bcnt, uint8_t* __restrict__ touch,
+           unsigned long long* ctr) {
+  const uint32_t nact = uint32_t(ctr_in[kActiveCount]);
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
+  for (uint32_t a = warp; a < nact; a += nwarps) {
+    const uint32_t u = act_list[a];
+    const uint64_t base = off[u];
+    const uint32_t U = cnt[u];
+    uint64_t* L = keys + base;
+    uint8_t* T = touch + base;
+    uint32_t nk = 0;
+    for (uint32_t i = 0; i < U; ++i) {
+      const uint64_t vk = L[i];
+      const uint32_t v_id = key_id(vk);
+      const bool v_fresh = key_fresh(vk);
+      const float v_dist = key_dist(vk);
+      const float* xv = x + uint64_t(v_id) * d;
+      bool keep = true;
+      uint32_t w_id = kNone;
+      float w_dist = 0.f;
+      bool any_need = false;
+      for (uint32_t k0 = 0; k0 < nk; k0 += 32) {
+        const uint32_t k = k0 + lane;
+        const bool valid = k < nk;
+        const uint64_t wk = valid ? L[k] : 0ull;
+        const bool need = valid && (v_fresh || key_fresh(wk));
+        float dvw = 0.f;
+        bool occl = false;
+        if (need) {
+          dvw = l2_exact<kVec4>(xv, x + uint64_t(key_id(wk)) * d, d);
+          occl = v_dist >= dvw;
+        }
+        const unsigned m_valid = __ballot_sync(0xffffffffu, valid);
+        const unsigned m_need = __ballot_sync(0xffffffffu, need);
+        const unsigned m_occ = __ballot_sync(0xffffffffu, occl);
+        if (m_occ) {
+          const int first = __ffs(m_occ) - 1;
+          const unsigned below = (1u << first) - 1u;  // lanes before occluder
+          if (lane == 0) {
+            checks += __popc(m_need & below) + 1;
+            skips += __popc(m_valid & ~m_need & below);
+          }
+          if (need && uint32_t(lane) <= uint32_t(first)) T[k] = 1;
+          w_id = key_id(__shfl_sync(0xffffffffu, wk, first));
+          w_dist = __shfl_sync(0xffffffffu, dvw, first);
+          any_need = true;
+          keep = false;
+          break;
+        }
+        if (lane == 0) {
+          checks += __popc(m_need);
+          skips += __popc(m_valid & ~m_need);
+        }
+        if (need) T[k] = 1;
+        any_need |= (m_need != 0);
+      }
+      if (lane == 0) {
+        if (any_need) T[i] = 1;
+        if (keep) {
+          L[nk] = vk;
+          pend_src[base + i] = kNone;
+        } else {
+          ++removed;
+          pend_src[base + i] = w_id;
+          pend_key[base + i] = make_key(w_dist, v_id, 1u);
+          atomicAdd(&bcnt[w_id], 1ull);
+        }
+      }
+      if (keep) ++nk;
+      __syncwarp();
+    }
+    // survivors are flagged old (builder.cpp:68)
+    for (uint32_t k = lane; k < nk; k += 32) L[k] &= ~1ull;
+    uint32_t t = 0;
+    for (uint32_t j = lane; j < U; j += 32) t += T[j];
+    touched += t;
+    if (lane == 0) post_cnt[u] = nk;
+    __syncwarp();
+  }
+  warp_add_counter(&ctr[kRemoved], removed);
+  warp_add_counter(&ctr[kPairChecks], checks);
+  warp_add_counter(&ctr[kFlagSkips], skips);
+  warp_add_counter(&ctr[kTouched], touched);
+}
+
+// Scatter emitted redirects into per-source buckets.
+__global__ void k_pend_scatter(uint64_t span, const uint32_t* __restrict__ pend_src,
+                               const uint64_t* __restrict__ pend_key,
+                               const uint64_t* __restrict__ boff,
+                               unsigned long long* __restrict__ bcur,
+                               uint64_t* __restrict__ bkey) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < span;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = pend_src[e];
+    if (s == kNone) continue;
+    const uint64_t pos = boff[s] + atomicAdd(&bcur[s], 1ull);
+    bkey[pos] = pend_key[e];
+  }
+}
+
+// Append-if-absent decisions (builder.cpp:117-136 / :236-243), one warp per
+// vertex.  A bucket entry is dropped when its id is already in the vertex's
+// post-scan list or (dedupe) when an earlier bucket entry carries the same
+// id: duplicate redirects carry bit-identical distances (l2 is evaluated as
+// l2(row v, row w) everywhere), so keeping any one of them equals the
+// reference's sort + unique.  new_cnt = post count + insertions.
+__global__ void __launch_bounds__(kBlock)
+    k_apply_count(uint64_t n, const uint64_t* __restrict__ off,
+                  const uint8_t* __restrict__ active,
+                  const uint64_t* __restrict__ key_a,
+                  const uint64_t* __restrict__ key_s,
+                  const uint32_t* __restrict__ post_cnt,
+                  const uint64_t* __restrict__ boff,
+                  const uint64_t* __restrict__ bkey, uint8_t* __restrict__ bflag,
+                  uint32_t* __restrict__ new_cnt, int dedupe,
+                  unsigned long long* __restrict__ ctr) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  unsigned long long inserted = 0;
+  for (uint64_t u = warp; u < n; u += nwarps) {
+    const uint64_t b0 = boff[u], b1 = boff[u + 1];
+    const uint32_t pc = post_cnt[u];
+    if (b0 == b1) {
+      if (lane == 0) new_cnt[u] = pc;
+      continue;
+    }
+    const uint64_t* P = (active && active[u] ? key_s : key_a) + off[u];
+    uint32_t ins = 0;
+    for (uint64_t xb = b0; xb < b1; xb += 32) {
+      const uint64_t xi = xb + lane;
+      if (xi < b1) {
+        const uint32_t id = key_id(bkey[xi]);
+        bool drop = false;
+        if (dedupe)
+          for (uint64_t y = b0; y < xi && !drop; ++y) drop = key_id(bkey[y]) == id;
+        for (uint32_t j = 0; j < pc && !drop; ++j) {
+          const uint64_t pk = P[j];
+          drop = pk != kTomb && key_id(pk) == id;
+        }
+        bflag[xi] = drop ? 1 : 0;
+        ins += drop ? 0 : 1;
+      }
+    }
+    ins = uint32_t(warp_sum(ins));
+    if (lane == 0) new_cnt[u] = pc + ins;
+    inserted += lane == 0 ? ins : 0;
+  }
+  if (lane == 0 && inserted) atomicAdd(&ctr[kInserted], inserted);
+}
+
+// Write the next CSR: each vertex's post list (tombstones dropped) followed
+// by its undropped bucket entries.  One warp per vertex, ballot compaction.
+__global__ void __launch_bounds__(kBlock)
+    k_rebuild(uint64_t n, const uint64_t* __restrict__ off,
+              const uint8_t* __restrict__ active,
+              const uint64_t* __restrict__ key_a,
+              const uint64_t* __restrict__ key_s,
+              const uint32_t* __restrict__ post_cnt,
+              const uint64_t* __restrict__ boff,
+              const uint64_t* __restrict__ bkey,
+              const uint8_t* __restrict__ bflag,
+              const uint64_t* __restrict__ off_b, uint64_t* __restrict__ key_b) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  for (uint64_t u = warp; u < n; u += nwarps) {
+    const uint64_t* P = (active && active[u] ? key_s : key_a) + off[u];
+    const uint32_t pc = post_cnt[u];
+    uint64_t* dst = key_b + off_b[u];
+    uint32_t w = 0;
+    for (uint32_t j0 = 0; j0 < pc; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint64_t k = j < pc ? P[j] : kTomb;
+      const bool live = k != kTomb;
+      const unsigned m = __ballot_sync(0xffffffffu, live);
+      if (live) dst[w + __popc(m & ((1u << lane) - 1))] = k;
+      w += __popc(m);
+    }
+    if (boff) {
+      const uint64_t b0 = boff[u], b1 = boff[u + 1];
+      for (uint64_t xb = b0; xb < b1; xb += 32) {
+        const uint64_t xi = xb + lane;
+        const bool live = xi < b1 && !bflag[xi];
+        const unsigned m = __ballot_sync(0xffffffffu, live);
+        if (live) dst[w + __popc(m & ((1u << lane) - 1))] = bkey[xi];
+        w += __popc(m);
+      }
+    }
+  }
+}
+
+// ----------------------------------------------------------- reverse phase
+// add_reverse_edges, builder.cpp:228-243: every edge u->v proposes v->u with
+// the same cached distance, flagged fresh, appended when absent.
+__global__ void __launch_bounds__(kBlock)
+    k_count_targets(uint64_t n, const uint64_t* __restrict__ off,
+                    const uint32_t* __restrict__ cnt,
+                    const uint64_t* __restrict__ key,
+                    unsigned long long* __restrict__ bcnt) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  for (uint64_t u = warp; u < n; u += nwarps) {
+    const uint64_t b = off[u];
+    const uint32_t U = cnt[u];
+    for (uint32_t j = lane; j < U; j += 32) atomicAdd(&bcnt[key_id(key[b + j])], 1ull);
+  }
+}
+
+// mode 0: reverse proposal key (dist, u, fresh); mode 1: in-edge key
+// (dist bits << 32 | source) with the edge slot as payload (in_prune).
+__global__ void __launch_bounds__(kBlock)
+    k_scatter_targets(uint64_t n, const uint64_t* __restrict__ off,
+                      const uint32_t* __restrict__ cnt,
+                      const uint64_t* __restrict__ key,
+                      const uint64_t* __restrict__ boff,
+                      unsigned long long* __restrict__ bcur,
+                      uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpay,
+                      int mode) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  for (uint64_t u = warp; u < n; u += nwarps) {
+    const uint64_t b = off[u];
+    const uint32_t U = cnt[u];
+    for (uint32_t j = lane; j < U; j += 32) {
+      const uint64_t k = key[b + j];
+      const uint32_t t = key_id(k);
+      const uint64_t pos = boff[t] + atomicAdd(&bcur[t], 1ull);
+      if (mode == 0) {
+        bkey[pos] = make_key(key_dist(k), uint32_t(u), 1u);
+      } else {
+        bkey[pos] = (uint64_t(key_dbits(k)) << 32) | uint64_t(u);
+        bpay[pos] = uint32_t(b + j);
+      }
+    }
+  }
+}
+
+// segment ends for "sort only lists longer than R" (out_prune) or all lists
+__global__ void k_seg_end(uint64_t n, const uint64_t* __restrict__ begin,
+                          const uint32_t* __restrict__ cnt,
+                          const uint64_t* __restrict__ boff, uint32_t R,
+                          uint64_t* __restrict__ seg_end) {
+  uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  uint64_t len = cnt ? cnt[u] : boff[u + 1] - boff[u];
+  seg_end[u] = begin[u] + (len > R ? len : 0);
+}
+
+// out_prune, builder.cpp:141-150: a list longer than R keeps its R nearest.
+__global__ void __launch_bounds__(kBlock)
+    k_out_take(uint64_t n, const uint64_t* __restrict__ off,
+               uint32_t* __restrict__ cnt, const uint64_t* __restrict__ key_s,
+               uint64_t* __restrict__ key, uint32_t R) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  for (uint64_t u = warp; u < n; u += nwarps) {
+    if (cnt[u] <= R) continue;
+    const uint64_t b = off[u];
+    for (uint32_t j = lane; j < R; j += 32) key[b + j] = key_s[b + j];
+    __syncwarp();
+    if (lane == 0) cnt[u] = R;
+  }
+}
+
+// in_prune, builder.cpp:162-176: in-edges of each target sorted by
+// (dist, source); ranks >= R are deleted from their source lists.
+__global__ void __launch_bounds__(kBlock)
+    k_in_mark(uint64_t n, const uint64_t* __restrict__ boff,
+              const uint32_t* __restrict__ bpay_s, uint64_t* __restrict__ key,
+              uint32_t R) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  for (uint64_t t = warp; t < n; t += nwarps) {
+    const uint64_t b0 = boff[t], b1 = boff[t + 1];
+    if (b1 - b0 <= R) continue;
+    for (uint64_t r = b0 + R + lane; r < b1; r += 32) key[bpay_s[r]] = kTomb;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_count_live(uint64_t n, const uint64_t* __restrict__ off,
+                 const uint32_t* __restrict__ cnt,
+                 const uint64_t* __restrict__ key, uint32_t* __restrict__ out) {
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t lane = lane_id();
+  for (uint64_t u = warp; u < n; u += nwarps) {
+    const uint64_t b = off[u];
+    const uint32_t U = cnt[u];
+    uint32_t live = 0;
+    for (uint32_t j = lane; j < U; j += 32) live += key[b + j] != kTomb;
+    live = uint32_t(warp_sum(live));
+    if (lane == 0) out[u] = live;
+  }
+}
+
+// ------------------------------------------------------------- host glue
+
+unsigned grid_for(uint64_t items, unsigned block, unsigned cap = 1u << 20) {
+  uint64_t g = (items + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return unsigned(g);
+}
+
+unsigned warp_grid(rnndg_ctx* c, uint64_t items) {
+  // one warp per item, persistent: enough blocks to fill every SM twice over
+  uint64_t need = (items + kWarpsPerBlock - 1) / kWarpsPerBlock;
+  uint64_t cap = uint64_t(sm_count(c)) * 16;
+  if (need < 1) need = 1;
+  return unsigned(need < cap ? need : cap);
+}
+
+void* cub_temp(rnndg_ctx* c, size_t bytes) {
+  return c->cub_tmp.ensure(bytes);
+}
+
+// exclusive scan of n u32 (or u64) counts into n+1 u64 offsets
+void scan_u32(rnndg_ctx* c, const uint32_t* in, uint64_t* out, uint64_t n) {
+  // out[n] must be the total: scan n+1 items with a zero appended through
+  // the transform iterator reading in[n] is out of bounds, so scan n items
+  // and add the last element with a tiny kernel-free trick: scan n+1 over a
+  // count array whose last slot is zero (callers size arrays n+1).
+  cub::TransformInputIterator<uint64_t, ToU64, const uint32_t*> it(in, ToU64{});
+  size_t bytes = 0;
+  RNNDG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, out, int64_t(n + 1), c->stream));
+  void* tmp = cub_temp(c, bytes);
+  RNNDG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, it, out, int64_t(n + 1), c->stream));
+  c->launches += 1;
+}
+
+void scan_u64(rnndg_ctx* c, const unsigned long long* in, uint64_t* out, uint64_t n) {
+  size_t bytes = 0;
+  const uint64_t* ip = reinterpret_cast<const uint64_t*>(in);
+  RNNDG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, ip, out, int64_t(n + 1), c->stream));
+  void* tmp = cub_temp(c, bytes);
+  RNNDG_CUDA(cub::DeviceScan::ExclusiveSum(tmp, bytes, ip, out, int64_t(n + 1), c->stream));
+  c->launches += 1;
+}
+
+// segments [begin[u], end[u]) of keys_in sorted ascending into keys_out
+void seg_sort_keys(rnndg_ctx* c, const uint64_t* keys_in, uint64_t* keys_out,
+                   uint64_t span, uint64_t nseg, const uint64_t* begin,
+                   const uint64_t* end) {
+  if (span == 0 || nseg == 0) return;
+  if (span > uint64_t(INT32_MAX)) throw CudaError("segmented sort span exceeds 2^31");
+  size_t bytes = 0;
+  RNNDG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, keys_in, keys_out,
+                                                int(span), int(nseg), begin, end,
+                                                c->stream));
+  void* tmp = cub_temp(c, bytes);
+  RNNDG_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp, bytes, keys_in, keys_out, int(span),
+                                                int(nseg), begin, end, c->stream));
+  c->launches += 3;
+}
+
+void seg_sort_pairs(rnndg_ctx* c, const uint64_t* kin, uint64_t* kout,
+                    const uint32_t* vin, uint32_t* vout, uint64_t span,
+                    uint64_t nseg, const uint64_t* begin, const uint64_t* end) {
+  if (span == 0 || nseg == 0) return;
+  if (span > uint64_t(INT32_MAX)) throw CudaError("segmented sort span exceeds 2^31");
+  size_t bytes = 0;
+  RNNDG_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, kin, kout, vin, vout,
+                                                 int(span), int(nseg), begin, end,
+                                                 c->stream));
+  void* tmp = cub_temp(c, bytes);
+  RNNDG_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp, bytes, kin, kout, vin, vout,
+                                                 int(span), int(nseg), begin, end,
+                                                 c->stream));
+  c->launches += 3;
+}
+
+uint64_t read_u64(rnndg_ctx* c, const uint64_t* dev) {
+  uint64_t v = 0;
+  RNNDG_CUDA(cudaMemcpyAsync(&v, dev, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  return v;
+}
+
+// Build graph B from (post lists, buckets) and make it the current graph.
+// new_cnt must already be in c->cnt_b.
+void rebuild_and_swap(rnndg_ctx* c, const uint8_t* active, const uint32_t* post_cnt,
+                      const uint64_t* boff, const uint64_t* bkey,
+                      const uint8_t* bflag) {
+  const uint64_t n = c->n;
+  c->off_b.ensure(n + 1);
+  scan_u32(c, c->cnt_b.p, c->off_b.p, n);
+  const uint64_t total = read_u64(c, c->off_b.p + n);
+  c->key_b.ensure(total ? total : 1);
+  RNNDG_LAUNCH(c, k_rebuild, warp_grid(c, n), kBlock, 0, n, c->off.p, active, c->key.p,
+               c->key_s.p, post_cnt, boff, bkey, bflag, c->off_b.p, c->key_b.p);
+  c->off.swap(c->off_b);
+  c->key.swap(c->key_b);
+  c->cnt.swap(c->cnt_b);
+  c->span = total;
+}
+
+void ensure_scratch(rnndg_ctx* c) {
+  const uint64_t n = c->n, span = c->span ? c->span : 1;
+  c->active.ensure(n);
+  c->act_list.ensure(n);
+  c->post_cnt.ensure(n + 1);
+  c->cnt_b.ensure(n + 1);
+  c->seg_end.ensure(n);
+  c->bcnt.ensure(n + 1);
+  c->bcur.ensure(n);
+  c->boff.ensure(n + 1);
+  c->counters.ensure(kNumCounters);
+  c->key_s.ensure(span);
+  c->pend_src.ensure(span);
+  c->pend_key.ensure(span);
+  c->touch.ensure(span);
+  c->bkey.ensure(span);
+  c->bflag.ensure(span);
+}
+
+template <class T>
+void zero(rnndg_ctx* c, T* p, uint64_t count, int value = 0) {
+  if (count) RNNDG_CUDA(cudaMemsetAsync(p, value, count * sizeof(T), c->stream));
+}
+
+float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
+  float ms = 0.f;
+  RNNDG_CUDA(cudaEventElapsedTime(&ms, a, b));
+  return ms;
+}
+
+}  // namespace
+
+int sm_count(rnndg_ctx* c) {
+  static thread_local int cached_dev = -1, cached = 0;
+  if (cached_dev != c->device) {
+    RNNDG_CUDA(cudaDeviceGetAttribute(&cached, cudaDevAttrMultiProcessorCount, c->device));
+    cached_dev = c->device;
+  }
+  return cached;
+}
+
+void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
+  const uint64_t n = c->n;
+  if (n < 2) throw ParamError("random_init: need at least 2 vectors");
+  if (S < 1 || S > n - 1) throw ParamError("random_init: S out of [1, n-1]");
+  c->span = n * S;
+  c->off.ensure(n + 1);
+  c->cnt.ensure(n + 1);
+  c->key.ensure(c->span);
+  RNNDG_LAUNCH(c, k_fill_offsets, grid_for(n + 1, 256), 256, 0, n, S, c->off.p, c->cnt.p);
+  if (c->d % 4 == 0)
+    RNNDG_LAUNCH(c, k_random_init<true>, warp_grid(c, n), kBlock, 0, n, S, seed, c->x,
+                 c->d, c->key.p);
+  else
+    RNNDG_LAUNCH(c, k_random_init<false>, warp_grid(c, n), kBlock, 0, n, S, seed, c->x,
+                 c->d, c->key.p);
+  c->has_graph = true;
+  c->has_distances = true;
+}
+
+void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_sort,
+                    double* t_apply, uint64_t* touched, uint64_t* active_entries) {
+  const uint64_t n = c->n;
+  ensure_scratch(c);
+  unsigned long long* ctr = c->counters.p;
+  zero(c, ctr, kNumCounters);
+  zero(c, c->pend_src.p, c->span, 0xFF);
+  zero(c, c->touch.p, c->span);
+  zero(c, c->bcnt.p, n + 1);
+  zero(c, c->bcur.p, n);
+  RNNDG_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p,
+               c->key.p, c->active.p, c->seg_end.p, c->act_list.p, c->post_cnt.p, ctr);
+  seg_sort_keys(c, c->key.p, c->key_s.p, c->span, n, c->off.p, c->seg_end.p);
+  RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
+  const unsigned scan_grid = unsigned(sm_count(c)) * 8;
+  if (c->d % 4 == 0)
+    RNNDG_LAUNCH(c, k_scan<true>, scan_grid, kBlock, 0, c->act_list.p, ctr, c->off.p,
+                 c->cnt.p, c->key_s.p, c->x, c->d, c->post_cnt.p, c->pend_src.p,
+                 c->pend_key.p, c->bcnt.p, c->touch.p, ctr);
+  else
+    RNNDG_LAUNCH(c, k_scan<false>, scan_grid, kBlock, 0, c->act_list.p, ctr, c->off.p,
+                 c->cnt.p, c->key_s.p, c->x, c->d, c->post_cnt.p, c->pend_src.p,
+                 c->pend_key.p, c->bcnt.p, c->touch.p, ctr);
+  RNNDG_CUDA(cudaEventRecord(c->ev[2], c->stream));
+  scan_u64(c, c->bcnt.p, c->boff.p, n);
+  RNNDG_LAUNCH(c, k_pend_scatter, grid_for(c->span, 256, 148 * 64), 256, 0, c->span,
+               c->pend_src.p, c->pend_key.p, c->boff.p, c->bcur.p, c->bkey.p);
+  RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->active.p,
+               c->key.p, c->key_s.p, c->post_cnt.p, c->boff.p, c->bkey.p, c->bflag.p,
+               c->cnt_b.p, 1, ctr);
+  rebuild_and_swap(c, c->active.p, c->post_cnt.p, c->boff.p, c->bkey.p, c->bflag.p);
+  RNNDG_CUDA(cudaEventRecord(c->ev[3], c->stream));
+  unsigned long long h[kNumCounters];
+  RNNDG_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  if (out) {
+    out->removed = h[kRemoved];
+    out->inserted = h[kInserted];
+    out->flag_skips = h[kFlagSkips];
+    out->pair_checks = h[kPairChecks];
+  }
+  if (t_sort) *t_sort += elapsed_ms(c->ev[0], c->ev[1]) * 1e-3;
+  if (t_scan) *t_scan += elapsed_ms(c->ev[1], c->ev[2]) * 1e-3;
+  if (t_apply) *t_apply += elapsed_ms(c->ev[2], c->ev[3]) * 1e-3;
+  if (touched) *touched += h[kTouched];
+  if (active_entries) *active_entries += h[kActiveEntries];
+}
+
+namespace {
+
+void out_prune(rnndg_ctx* c, uint32_t R) {
+  const uint64_t n = c->n;
+  RNNDG_LAUNCH(c, k_seg_end, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, nullptr, R,
+               c->seg_end.p);
+  seg_sort_keys(c, c->key.p, c->key_s.p, c->span, n, c->off.p, c->seg_end.p);
+  RNNDG_LAUNCH(c, k_out_take, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
+               c->key_s.p, c->key.p, R);
+}
+
+void in_prune(rnndg_ctx* c, uint32_t R) {
+  const uint64_t n = c->n;
+  zero(c, c->bcnt.p, n + 1);
+  zero(c, c->bcur.p, n);
+  RNNDG_LAUNCH(c, k_count_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
+               c->key.p, c->bcnt.p);
+  scan_u64(c, c->bcnt.p, c->boff.p, n);
+  const uint64_t m = read_u64(c, c->boff.p + n);
+  c->bkey.ensure(m ? m : 1);
+  c->bkey_s.ensure(m ? m : 1);
+  c->bpay.ensure(m ? m : 1);
+  c->bpay_s.ensure(m ? m : 1);
+  RNNDG_LAUNCH(c, k_scatter_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
+               c->key.p, c->boff.p, c->bcur.p, c->bkey.p, c->bpay.p, 1);
+  RNNDG_LAUNCH(c, k_seg_end, grid_for(n, 256), 256, 0, n, c->boff.p, nullptr, c->boff.p, R,
+               c->seg_end.p);
+  seg_sort_pairs(c, c->bkey.p, c->bkey_s.p, c->bpay.p, c->bpay_s.p, m, n, c->boff.p,
+                 c->seg_end.p);
+  RNNDG_LAUNCH(c, k_in_mark, warp_grid(c, n), kBlock, 0, n, c->boff.p, c->bpay_s.p,
+               c->key.p, R);
+  RNNDG_LAUNCH(c, k_count_live, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
+               c->key.p, c->cnt_b.p);
+  rebuild_and_swap(c, nullptr, c->cnt.p, nullptr, nullptr, nullptr);
+}
+
+}  // namespace
+
+void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
+  if (R < 1) throw ParamError("add_reverse_edges: R must be >= 1");
+  if (!c->has_distances) throw ParamError("add_reverse_edges: graph has no distances");
+  const uint64_t n = c->n;
+  ensure_scratch(c);
+  // 1. reversals bucketed by their source (= target of the forward edge)
+  zero(c, c->bcnt.p, n + 1);
+  zero(c, c->bcur.p, n);
+  RNNDG_LAUNCH(c, k_count_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
+               c->key.p, c->bcnt.p);
+  scan_u64(c, c->bcnt.p, c->boff.p, n);
+  const uint64_t m = read_u64(c, c->boff.p + n);
+  c->bkey.ensure(m ? m : 1);
+  c->bflag.ensure(m ? m : 1);
+  RNNDG_LAUNCH(c, k_scatter_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
+               c->key.p, c->boff.p, c->bcur.p, c->bkey.p, nullptr, 0);
+  // 2. append-if-absent (no duplicates among reversals: edges are unique)
+  RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, nullptr,
+               c->key.p, nullptr, c->cnt.p, c->boff.p, c->bkey.p, c->bflag.p,
+               c->cnt_b.p, 0, c->counters.p);
+  rebuild_and_swap(c, nullptr, c->cnt.p, c->boff.p, c->bkey.p, c->bflag.p);
+  ensure_scratch(c);  // span grew
+  // 3. degree caps (builder.cpp:244-250)
+  if (order == RNNDG_OUT_THEN_IN) {
+    out_prune(c, R);
+    in_prune(c, R);
+  } else {
+    in_prune(c, R);
+    ensure_scratch(c);
+    out_prune(c, R);
+  }
+}
+
+void op_sort_lists(rnndg_ctx* c) {
+  const uint64_t n = c->n;
+  ensure_scratch(c);
+  RNNDG_LAUNCH(c, k_seg_end, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, nullptr, 0u,
+               c->seg_end.p);
+  seg_sort_keys(c, c->key.p, c->key_s.p, c->span, n, c->off.p, c->seg_end.p);
+  c->key.swap(c->key_s);
+}
+
+}  // namespace rnndg

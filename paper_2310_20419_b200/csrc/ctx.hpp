@@ -1,0 +1,154 @@
+// ctx.hpp -- the rnndg_ctx definition and device buffer plumbing (host side).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "rnndg.h"
+
+namespace rnndg {
+
+// A failed CUDA call or an internal invariant: surfaces as RNNDG_EINTERNAL.
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+// rnnd::ParamError analogue (common.hpp:21-23): RNNDG_EPARAM.
+struct ParamError : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+// rnnd::DataError analogue (common.hpp:16-18): RNNDG_EDATA.
+struct DataError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define RNNDG_CUDA(call)                                                     \
+  do {                                                                       \
+    cudaError_t e_ = (call);                                                 \
+    if (e_ != cudaSuccess)                                                   \
+      throw ::rnndg::CudaError(std::string(#call) + ": " +                   \
+                               cudaGetErrorString(e_) + " at " + __FILE__ +  \
+                               ":" + std::to_string(__LINE__));              \
+  } while (0)
+
+// Grow-only device allocation.  ensure() discards contents when it grows.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t cap = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+  }
+  T* ensure(size_t n) {
+    if (n <= cap && p) return p;
+    release();
+    size_t want = n < 16 ? 16 : n + n / 8;  // headroom against regrowth
+    RNNDG_CUDA(cudaMalloc(&p, want * sizeof(T)));
+    cap = want;
+    return p;
+  }
+  void swap(DevBuf& o) {
+    std::swap(p, o.p);
+    std::swap(cap, o.cap);
+  }
+};
+
+// Device-side counters of one pass (reduced with atomics).
+enum Counter : int {
+  kRemoved = 0,
+  kInserted,
+  kFlagSkips,
+  kPairChecks,
+  kTouched,
+  kActiveEntries,
+  kActiveCount,
+  kNumCounters
+};
+
+}  // namespace rnndg
+
+struct rnndg_ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  std::string err;
+  uint64_t launches = 0;
+
+  // VectorStore (vector_store.hpp:12-20), row-major n x d fp32
+  rnndg::DevBuf<float> x_own;
+  const float* x = nullptr;
+  uint64_t n = 0;
+  uint32_t d = 0;
+
+  // Graph "A": lists at key[off[u] .. off[u] + cnt[u]).  off is monotone and
+  // may leave gaps between lists (capacity layout); span = off[n].
+  rnndg::DevBuf<uint64_t> off, off_b;
+  rnndg::DevBuf<uint32_t> cnt, cnt_b;
+  rnndg::DevBuf<uint64_t> key, key_b, key_s;
+  uint64_t span = 0;
+  bool has_graph = false;
+  bool has_distances = true;
+
+  // pass scratch
+  rnndg::DevBuf<uint8_t> active, touch, bflag;
+  rnndg::DevBuf<uint32_t> act_list, pend_src, bpay, bpay_s;
+  rnndg::DevBuf<uint64_t> pend_key, bkey, bkey_s, seg_end, boff;
+  rnndg::DevBuf<unsigned long long> bcnt, bcur;
+  rnndg::DevBuf<uint32_t> post_cnt;
+  rnndg::DevBuf<unsigned long long> counters;
+  rnndg::DevBuf<unsigned char> cub_tmp;
+
+  // eval scratch
+  rnndg::DevBuf<float> q_dev;
+  rnndg::DevBuf<uint32_t> ids_dev, entry_dev, seen_bits;
+  rnndg::DevBuf<float> dists_dev;
+  rnndg::DevBuf<unsigned long long> qstat_dev;
+
+  std::vector<rnndg_counts> pass_counts;
+  // timing events
+  cudaEvent_t ev[8] = {};
+};
+
+namespace rnndg {
+
+// launch bookkeeping: every kernel of this library goes through this
+#define RNNDG_LAUNCH(ctx, kernel, grid, block, smem, ...)                     \
+  do {                                                                      \
+    kernel<<<(grid), (block), (smem), (ctx)->stream>>>(__VA_ARGS__);         \
+    ++(ctx)->launches;                                                      \
+    RNNDG_CUDA(cudaGetLastError());                                         \
+  } while (0)
+
+// build.cu
+void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed);
+void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan,
+                    double* t_sort, double* t_apply, uint64_t* touched,
+                    uint64_t* active_entries);
+void op_reverse(rnndg_ctx* c, uint32_t R, int order);
+void op_sort_lists(rnndg_ctx* c);
+int sm_count(rnndg_ctx* c);
+
+// eval.cu
+void op_search(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t L,
+               uint32_t K, uint32_t k, int entry_mode, uint32_t entry_vertex,
+               uint32_t entry_count, uint64_t seed, uint32_t* ids, float* dists,
+               uint64_t* visited, uint64_t* dist_comps);
+void op_brute_force(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t k,
+                    uint32_t* ids);
+void op_l2_pairs(rnndg_ctx* c, const uint32_t* a, const uint32_t* b,
+                 uint64_t npairs, float* out);
+uint32_t op_rng_strategy(rnndg_ctx* c, uint32_t u, const uint32_t* cand_ids,
+                         const float* cand_dists, uint32_t ncand,
+                         uint32_t* kept_ids, float* kept_dists);
+void op_degree_stats(rnndg_ctx* c, uint32_t cap, uint64_t out[3]);
+
+}  // namespace rnndg

@@ -1,0 +1,79 @@
+"""C-ABI library: loads without a GPU, exports every symbol include/rnndg.h
+declares, and its host-only pieces (seeded generators) are deterministic."""
+import hashlib
+import os
+import re
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "rnndg.h")).read()
+    return sorted(set(re.findall(r"\b(rnndg_[a-z0-9_]+)\s*\(", src)) - {"rnndg_progress_fn"})
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_2310_20419_b200 import _lib
+    L = _lib.lib()
+    syms = header_symbols()
+    assert len(syms) >= 20
+    for s in syms:
+        assert hasattr(L, s), s
+    assert sorted(_lib.EXPORTED) == syms
+
+
+def test_library_is_sm100a():
+    """The product .so carries sm_100a SASS (cuobjdump lists the ELF)."""
+    import shutil
+    import subprocess
+    from paper_2310_20419_b200 import _lib
+    exe = shutil.which("cuobjdump") or "/usr/local/cuda/bin/cuobjdump"
+    if not os.path.exists(exe):
+        return
+    out = subprocess.run([exe, "--list-elf", _lib.LIB_PATH], capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_create_without_gpu_reports_error_code():
+    import ctypes as C
+    import torch
+    from paper_2310_20419_b200 import _lib
+    if torch.cuda.is_available():
+        return
+    h = C.c_void_p()
+    rc = _lib.lib().rnndg_create(C.byref(h), 0)
+    assert rc in (_lib.EPARAM, _lib.EINTERNAL) and not h.value
+
+
+def test_datagen_deterministic_and_prefix_stable():
+    from paper_2310_20419_b200 import datagen as D
+    for c in (D.C1, D.C2, D.C3, D.C4, D.C5):
+        a = D.rows(c.cfg, c.seed, 0, 64)
+        b = D.rows(c.cfg, c.seed, 0, 64)
+        assert np.array_equal(a, b)
+        assert np.array_equal(D.rows(c.cfg, c.seed, 40, 24), a[40:])  # row-addressable
+        assert a.shape[1] == c.d and np.all(np.isfinite(a))
+
+
+def test_datagen_value_ranges():
+    from paper_2310_20419_b200 import datagen as D
+    x = D.base(D.C2, 4000)
+    assert x.min() == 0 and x.max() <= 255 and np.all(x == np.round(x))
+    assert 0.3 < float((x == 0).mean()) < 0.5  # ~40% zeros
+    x = D.base(D.C3, 2000)
+    assert x.min() >= 0 and x.max() <= 1
+    for c in (D.C4, D.C5):
+        x = D.base(c, 2000)
+        assert np.allclose(np.linalg.norm(x, axis=1), 1, atol=1e-5)
+
+
+def test_datagen_pinned_bytes():
+    """Generator drift would silently change every benchmark input."""
+    from paper_2310_20419_b200 import datagen as D
+    got = {c.name: hashlib.sha256(D.rows(c.cfg, c.seed, 0, 256).tobytes()).hexdigest()[:16]
+           for c in (D.C1, D.C2, D.C3, D.C4, D.C5)}
+    path = os.path.join(ROOT, "tests", "golden", "datagen_sha.txt")
+    want = dict(l.split() for l in open(path).read().splitlines() if l.strip())
+    assert got == want
