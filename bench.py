@@ -1,0 +1,338 @@
+"""Benchmark: RNN-Descent graph build on B200 (BASELINE.json metric).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config C3-gistlike-1M] [--n ROWS]
+
+One step = one full build (random init -> T1 x T2 update passes + reverse
+phases -> final sort; S=20 R=96 T1=4 T2=15) over the config's synthetic
+store already resident in HBM.  value = L2 dist-evals/s = pair checks
+(EditCounts::pair_checks, builder.cpp:57) summed over all ranks / max-rank
+device time.  e2e = the same metric through the C ABI with host buffers
+(H2D of the store, build, D2H of the graph) in the timed region.
+
+--impl reference runs the UNMODIFIED reference (oracle/_ref, rnnd::build with
+all host threads) on a bounded prefix sample of the same store.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
+HBM_FALLBACK_GBS = 6650.0
+CPU_SAMPLE_ROWS = 50_000
+METRIC = "RNN-Descent build L2 dist-evals/s (1M x 960 fp32, S=20 R=96 T1=4 T2=15)"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3-gistlike-1M")
+    ap.add_argument("--n", type=int, default=0, help="override rows (debug only)")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-recall", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_ROWS)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def hbm_peak():
+    try:
+        with open(PEAKS_PATH) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return HBM_FALLBACK_GBS, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
+                          if r[2 + i].lower().startswith("active")})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def store_rows(cfg, n):
+    from paper_2310_20419_b200 import datagen
+    return datagen.rows(cfg.cfg, cfg.seed, 0, n)
+
+
+# ------------------------------------------------------------ reference arm
+
+def run_reference(args, rank, world):
+    """The reference's own CPU implementation (oracle/_ref) on a bounded
+    sample; rank 0 only."""
+    if rank != 0:
+        return
+    from oracle import oracle as O
+    from paper_2310_20419_b200 import datagen
+    cfg = datagen.CONFIGS[args.config]
+    n = min(args.cpu_sample, cfg.n)
+    data = store_rows(cfg, n)
+    if not O.ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
+        return
+    cores = int(O.ref_lib().ref_max_threads())
+    g = O.RefGraph(data)
+    for _ in range(args.warmup):
+        g.build(threads=0)
+    secs, checks = [], []
+    for _ in range(args.steps):
+        rc, st = g.build(threads=0)
+        assert rc == 0
+        secs.append(float(st[0]))
+        checks.append(float(st[6]))
+    value = sum(checks) / sum(secs)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "dist-evals/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded generator, csrc/datagen.cpp)",
+        "config": {"workload": cfg.name, "rows": cfg.n, "dim": cfg.d, "sample_rows": n,
+                   "S": 20, "R": 96, "T1": 4, "T2": 15},
+        "cpu_baseline": {"value": value, "unit": "dist-evals/s", "cores": cores,
+                         "kind": "reference",
+                         "sample": f"rnnd::build(threads={cores}) on the first {n} rows of "
+                                   f"{cfg.name}"},
+        "e2e": {"value": value, "unit": "dist-evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "build_seconds": statistics.median(secs),
+    }
+    print(json.dumps(line))
+
+
+# ------------------------------------------------------------------ our arm
+
+def cpu_baseline(cfg, sample):
+    from oracle import oracle as O
+    n = min(sample, cfg.n)
+    data = store_rows(cfg, n)
+    if O.ref_available():
+        g = O.RefGraph(data)
+        rc, st = g.build(threads=0)
+        cores = int(O.ref_lib().ref_max_threads())
+        return {"value": float(st[6]) / float(st[0]), "unit": "dist-evals/s", "cores": cores,
+                "kind": "reference", "seconds": float(st[0]),
+                "sample": f"rnnd::build(threads={cores}) on the first {n} rows of {cfg.name}"}
+    g = O.OracleGraph(data)
+    t = time.perf_counter()
+    rc, pc = g.build()
+    dt = time.perf_counter() - t
+    return {"value": float(pc[:, 3].sum()) / dt, "unit": "dist-evals/s", "cores": 1,
+            "kind": "port", "seconds": dt,
+            "sample": f"C oracle build (1 thread) on the first {n} rows of {cfg.name}"}
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2310_20419_b200 import _lib, datagen
+    from paper_2310_20419_b200 import rnnd as R
+
+    cfg = datagen.CONFIGS[args.config]
+    n = args.n or cfg.n
+    data = store_rows(cfg, n)
+    store = R.VectorStore(data)
+    dev = R.Device(local)
+    dev.set_data(store)  # resident in HBM before the timed region
+    params = R.BuildParams()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            torch.distributed.barrier()
+
+    for _ in range(args.warmup):
+        R.build(store, params, device=dev)
+    barrier()
+    launches0 = dev.launches()
+    stats = []
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st = R.BuildStats()
+            g = R.build(store, params, st, device=dev)
+            stats.append(st)
+        barrier()
+        wall = time.perf_counter() - t0
+    launches = dev.launches() - launches0
+    dev_secs = sum(s.seconds for s in stats)
+    checks = sum(s.edits.pair_checks for s in stats)
+    t_rank = torch.tensor([dev_secs, float(checks)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        mx = t_rank.clone()
+        torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
+        torch.distributed.all_reduce(t_rank[1:], op=torch.distributed.ReduceOp.SUM)
+        t_rank[0] = mx[0]
+    max_secs, all_checks = float(t_rank[0]), float(t_rank[1])
+    value = all_checks / max_secs
+
+    # roofline of the distance stage: B = 4 d T + 24 A bytes
+    st0 = stats[-1]
+    alg_bytes = 4.0 * cfg.d * st0.touched + 24.0 * st0.active_entries
+    achieved = alg_bytes / st0.scan_seconds / 1e9
+    peak, peak_src = hbm_peak()
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "scan_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            if tj.get("config") == cfg.name:
+                traffic = tj.get("traffic_bytes_per_build")
+        except Exception:
+            traffic = None
+
+    # end to end through the C ABI with host buffers (H2D, build, D2H)
+    e2e = None
+    if rank == 0 or world > 1:
+        pinned = torch.empty(data.shape, dtype=torch.float32, pin_memory=True)
+        pinned.numpy()[:] = data
+        pstore = R.VectorStore(pinned.numpy())
+        e2e_secs, e2e_checks, d2h = 0.0, 0, 0
+        for _ in range(args.steps):
+            edev = dev
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            edev.set_data(pstore)  # H2D
+            st = R.BuildStats()
+            g = R.build(pstore, params, st, device=edev)
+            csr = edev.get_graph()  # D2H
+            e2e_secs += time.perf_counter() - t
+            e2e_checks += st.edits.pair_checks
+            d2h = int(csr.offsets.nbytes + 12 * len(csr.ids))
+        e2e = {"value": e2e_checks / e2e_secs, "unit": "dist-evals/s",
+               "h2d_bytes_per_step": int(data.nbytes), "d2h_bytes_per_step": d2h,
+               "seconds_per_step": e2e_secs / args.steps}
+
+    recall = None
+    if rank == 0 and not args.no_recall:
+        nq = min(cfg.nq, 1000)
+        q = datagen.rows(cfg.cfg, cfg.seed, cfg.n, nq) if n == cfg.n else \
+            datagen.rows(cfg.cfg, cfg.seed, n, nq)
+        qs = R.VectorStore(q)
+        t = time.perf_counter()
+        gt = R.brute_force_gt(store, qs, 10, device=dev)
+        t_gt = time.perf_counter() - t
+        g = R.build(store, params, device=dev)
+        recall = {"queries": nq, "gt_seconds": t_gt}
+        for L in (16, 32, 64):
+            timing = R.BatchTiming()
+            res = R.batch_search(g, store, qs, R.SearchParams(L=L, K=0, k=10), timing=timing)
+            recall[f"L{L}"] = {"recall@1": R.recall_at_1(res, R.GroundTruth(10, gt.ids), store, qs),
+                               "recall@10": R.recall_at_k(res, gt, 10), "qps": timing.qps}
+        deg = R.degree_stats(g)
+        recall["aod"] = deg.avg_out
+        recall["max_out"] = deg.max_out
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        cpu = cpu_baseline(cfg, args.cpu_sample)
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "dist-evals/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * max_secs / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator, csrc/datagen.cpp; stands in for GIST1M)",
+            "config": {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96,
+                       "T1": 4, "T2": 15, "parallelism": "replicas" if world > 1 else "1gpu",
+                       "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},
+            "build_seconds": max_secs / args.steps,
+            "wall_seconds_timed": wall,
+            "pair_checks_per_build": stats[-1].edits.pair_checks,
+            "stage_seconds": {"scan": st0.scan_seconds, "sort": st0.sort_seconds,
+                              "apply": st0.apply_seconds, "reverse": st0.reverse_seconds},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic,
+                         "kernel": "k_scan (distance stage)",
+                         "algorithmic_bytes_per_build": alg_bytes,
+                         "touched": st0.touched, "active_entries": st0.active_entries,
+                         "peak_source": peak_src},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "recall": recall,
+        }
+        print(json.dumps(line))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

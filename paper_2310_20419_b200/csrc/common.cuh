@@ -91,8 +91,9 @@ __device__ __forceinline__ float l2_finish(float s0, float s1, float s2,
   return __fadd_rn(__fadd_rn(s0, s1), __fadd_rn(s2, s3));
 }
 
-// Generic pointers; `vec4` when both rows are 16-byte aligned and the row
-// length is a multiple of 4 (the store guarantees this when d % 4 == 0).
+// `a` may point anywhere (global or shared: plain loads); `b` must be a
+// global row (read-only path).  `kVec4` when both rows are 16-byte aligned
+// and the row length is a multiple of 4 (true for every row when d % 4 == 0).
 template <bool kVec4>
 __device__ __forceinline__ float l2_exact(const float* __restrict__ a,
                                           const float* __restrict__ b,
@@ -104,18 +105,18 @@ __device__ __forceinline__ float l2_exact(const float* __restrict__ a,
     const float4* b4 = reinterpret_cast<const float4*>(b);
     const uint32_t d4 = d >> 2;
 #pragma unroll 4
-    for (uint32_t q = 0; q < d4; ++q) l2_step4(__ldg(a4 + q), __ldg(b4 + q), s0, s1, s2, s3);
+    for (uint32_t q = 0; q < d4; ++q) l2_step4(a4[q], __ldg(b4 + q), s0, s1, s2, s3);
     i = d4 << 2;
   } else {
     for (; i + 4 <= d; i += 4) {
-      float4 x = make_float4(__ldg(a + i), __ldg(a + i + 1), __ldg(a + i + 2), __ldg(a + i + 3));
+      float4 x = make_float4(a[i], a[i + 1], a[i + 2], a[i + 3]);
       float4 y = make_float4(__ldg(b + i), __ldg(b + i + 1), __ldg(b + i + 2), __ldg(b + i + 3));
       l2_step4(x, y, s0, s1, s2, s3);
     }
   }
   float sum = l2_finish(s0, s1, s2, s3);
   for (; i < d; ++i) {
-    float t = __fsub_rn(__ldg(a + i), __ldg(b + i));
+    float t = __fsub_rn(a[i], __ldg(b + i));
     sum = __fadd_rn(sum, __fmul_rn(t, t));
   }
   return sum;

@@ -49,7 +49,8 @@ struct SearchArgs {
 };
 
 template <bool kVec4>
-__device__ void consider_batch(const SearchArgs& a, const float* q,
+__device__ void consider_batch(const float* __restrict__ x, uint32_t d, uint32_t L,
+                               const float* q,
                                const uint32_t* cand, uint32_t m, uint32_t* seen,
                                uint64_t* pool, uint8_t* expd, uint32_t& psize,
                                unsigned long long& comps) {
@@ -64,7 +65,7 @@ __device__ void consider_batch(const SearchArgs& a, const float* q,
       const uint32_t old = atomicOr(&seen[id >> 5], bit);
       if (!(old & bit)) {
         fresh = true;
-        const float dist = l2_exact<kVec4>(q, a.x + uint64_t(id) * a.d, a.d);
+        const float dist = l2_exact<kVec4>(q, x + uint64_t(id) * d, d);
         ck = (uint64_t(__float_as_uint(dist)) << 32) | id;
       }
     }
@@ -74,14 +75,14 @@ __device__ void consider_batch(const SearchArgs& a, const float* q,
       const int src = __ffs(mask) - 1;
       mask &= mask - 1;
       const uint64_t key = __shfl_sync(0xffffffffu, ck, src);
-      if (psize == a.L && !(key < pool[psize - 1])) continue;  // rejected
+      if (psize == L && !(key < pool[psize - 1])) continue;  // rejected
       // upper_bound position: number of pool keys <= key (keys are unique)
       uint32_t pos = 0;
       for (uint32_t p0 = 0; p0 < psize; p0 += 32) {
         const uint32_t p = p0 + lane;
         pos += __popc(__ballot_sync(0xffffffffu, p < psize && pool[p] < key));
       }
-      const uint32_t last = psize < a.L ? psize : a.L - 1;  // new last index
+      const uint32_t last = psize < L ? psize : L - 1;  // new last index
       // shift [pos, last) right by one, from the top down in warp-wide steps
       for (int32_t hi = int32_t(last) - 1; hi >= int32_t(pos); hi -= 32) {
         const int32_t p = hi - int32_t(lane);
@@ -104,7 +105,7 @@ __device__ void consider_batch(const SearchArgs& a, const float* q,
         expd[pos] = 0;
       }
       __syncwarp();
-      if (psize < a.L) ++psize;
+      if (psize < L) ++psize;
     }
   }
 }
@@ -131,10 +132,13 @@ __global__ void k_search(SearchArgs a) {
     __syncwarp();
     uint32_t psize = 0;
     unsigned long long comps = 0, visited = 0;
+    __shared__ uint32_t entry_buf[1];
+    if (lane == 0) entry_buf[0] = a.entry_vertex;
+    __syncwarp();
     if (a.fixed)
-      consider_batch<kVec4>(a, q, &a.entry_vertex, 1, seen, pool, expd, psize, comps);
+      consider_batch<kVec4>(a.x, a.d, a.L, q, entry_buf, 1, seen, pool, expd, psize, comps);
     else
-      consider_batch<kVec4>(a, q, a.entries, a.nentries, seen, pool, expd, psize, comps);
+      consider_batch<kVec4>(a.x, a.d, a.L, q, a.entries, a.nentries, seen, pool, expd, psize, comps);
     for (;;) {
       uint32_t at = psize;
       for (uint32_t p0 = 0; p0 < psize; p0 += 32) {
@@ -166,7 +170,7 @@ __global__ void k_search(SearchArgs a) {
         ids_buf[lane] = id;
         __syncwarp();
         const uint32_t m = take - j0 < 32 ? take - j0 : 32;
-        consider_batch<kVec4>(a, q, ids_buf, m, seen, pool, expd, psize, comps);
+        consider_batch<kVec4>(a.x, a.d, a.L, q, ids_buf, m, seen, pool, expd, psize, comps);
       }
     }
     const uint32_t take = a.k < psize ? a.k : psize;
