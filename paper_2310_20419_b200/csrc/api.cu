@@ -3,6 +3,7 @@
 // reference's error classes, and runs the work on the context's device.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -93,7 +94,12 @@ int rnndg_create(rnndg_ctx** out, int device) {
     if (device < 0 || device >= ndev) throw ParamError("rnndg_create: no such device");
     RNNDG_CUDA(cudaSetDevice(device));
     RNNDG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    RNNDG_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    RNNDG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+    RNNDG_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     for (auto& e : c->ev) RNNDG_CUDA(cudaEventCreate(&e));
+    const char* tr = std::getenv("RNNDG_TRACE");
+    c->trace = tr && tr[0] == '1';
   } catch (const ParamError&) {
     delete c;
     return RNNDG_EPARAM;
@@ -111,6 +117,10 @@ int rnndg_destroy(rnndg_ctx* c) {
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& e : c->ev)
     if (e) cudaEventDestroy(e);
+  if (c->side) cudaStreamSynchronize(c->side);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_join) cudaEventDestroy(c->ev_join);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return RNNDG_OK;
@@ -131,6 +141,7 @@ int rnndg_set_data(rnndg_ctx* c, const float* rows, uint64_t n, uint32_t d) {
     c->n = n;
     c->d = d;
     c->has_graph = false;
+    c->xp_src = nullptr;  // chain-blocked copy is stale
   });
 }
 
@@ -145,6 +156,7 @@ int rnndg_set_data_device(rnndg_ctx* c, const float* rows_dev, uint64_t n, uint3
     c->n = n;
     c->d = d;
     c->has_graph = false;
+    c->xp_src = nullptr;
   });
 }
 
@@ -196,6 +208,7 @@ int rnndg_build(rnndg_ctx* c, uint32_t S, uint32_t R, uint32_t T1, uint32_t T2,
     const uint64_t launches0 = c->launches;
     c->pass_counts.clear();
     RNNDG_CUDA(cudaEventRecord(c->ev[4], c->stream));
+    c->xp_src = nullptr;  // the chain-blocked store copy is rebuilt inside the timed build
     op_random_init(c, S, seed);
     for (uint32_t t1 = 1; t1 <= T1; ++t1) {
       rnndg_counts outer{};

@@ -25,6 +25,9 @@
 
 #include "common.cuh"
 #include "ctx.hpp"
+#include "scan.cuh"
+
+#include <cstdio>
 
 namespace rnndg {
 
@@ -123,128 +126,33 @@ __global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
     seg_end[u] = act ? b + U : b;
     if (act) {
       aentries = U;
+      atomicMax(&ctr[kMaxLen], (unsigned long long)U);
     } else {
       post_cnt[u] = U;
       skips = (unsigned long long)U * (U ? U - 1 : 0) / 2;
     }
   }
-  // warp-aggregated append of active ids
-  unsigned mask = __ballot_sync(0xffffffffu, act);
-  uint32_t base = 0;
-  if (lane_id() == 0 && mask)
-    base = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kActiveCount]), __popc(mask));
-  base = __shfl_sync(0xffffffffu, base, 0);
-  if (act) act_list[base + __popc(mask & ((1u << lane_id()) - 1))] = uint32_t(u);
+  // warp-aggregated append of active ids: lists that fit the CTA scan's
+  // shared-memory arrays go to act_list[0..), longer ones to act_list[n..)
+  const bool small = act && cnt[u < n ? u : 0] <= kScanUcap;
+  const bool large = act && !small;
+  const unsigned ms = __ballot_sync(0xffffffffu, small);
+  const unsigned ml = __ballot_sync(0xffffffffu, large);
+  uint32_t bs = 0, bl = 0;
+  if (lane_id() == 0) {
+    if (ms) bs = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kActiveCount]), __popc(ms));
+    if (ml) bl = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLargeCount]), __popc(ml));
+  }
+  bs = __shfl_sync(0xffffffffu, bs, 0);
+  bl = __shfl_sync(0xffffffffu, bl, 0);
+  const unsigned below = (1u << lane_id()) - 1;
+  if (small) act_list[bs + __popc(ms & below)] = uint32_t(u);
+  if (large) act_list[n + bl + __popc(ml & below)] = uint32_t(u);
   warp_add_counter(&ctr[kFlagSkips], skips);
   warp_add_counter(&ctr[kActiveEntries], aentries);
 }
 
-// ------------------------------------------------------------------- scan
-// scan_vertex, builder.cpp:45-69, one warp per active vertex.  The list is
-// already sorted by (dist, id).  Kept entries are compacted in place to the
-// front of the list (kept position <= candidate position), so the kept list
-// K is read back from L1/L2.  For candidate v the warp evaluates up to 32
-// kept entries at once (one lane per pair, exact L2) and takes the FIRST
-// occluder in K order via ballot, which reproduces the reference's early
-// break and its exact pair_checks / flag_skips counts.
-//
-// A removed candidate at sorted slot s emits the redirect (w, v, d(v,w)) into
-// pend_src/pend_key[s] and bumps the bucket count of w.
-template <bool kVec4>
-__global__ void __launch_bounds__(kBlock)
-    k_scan(const uint32_t* __restrict__ act_list,
-           const unsigned long long* ctr_in,
-           const uint64_t* __restrict__ off, const uint32_t* __restrict__ cnt,
-           uint64_t* __restrict__ keys, const float* __restrict__ x,
-           uint32_t d, uint32_t* __restrict__ post_cnt,
-           uint32_t* __restrict__ pend_src, uint64_t* __restrict__ pend_key,
-           unsigned long long* __restrict__ bcnt, uint8_t* __restrict__ touch,
-           unsigned long long* ctr) {
-  const uint32_t nact = uint32_t(ctr_in[kActiveCount]);
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t lane = lane_id();
-  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
-  for (uint32_t a = warp; a < nact; a += nwarps) {
-    const uint32_t u = act_list[a];
-    const uint64_t base = off[u];
-    const uint32_t U = cnt[u];
-    uint64_t* L = keys + base;
-    uint8_t* T = touch + base;
-    uint32_t nk = 0;
-    for (uint32_t i = 0; i < U; ++i) {
-      const uint64_t vk = L[i];
-      const uint32_t v_id = key_id(vk);
-      const bool v_fresh = key_fresh(vk);
-      const float v_dist = key_dist(vk);
-      const float* xv = x + uint64_t(v_id) * d;
-      bool keep = true;
-      uint32_t w_id = kNone;
-      float w_dist = 0.f;
-      bool any_need = false;
-      for (uint32_t k0 = 0; k0 < nk; k0 += 32) {
-        const uint32_t k = k0 + lane;
-        const bool valid = k < nk;
-        const uint64_t wk = valid ? L[k] : 0ull;
-        const bool need = valid && (v_fresh || key_fresh(wk));
-        float dvw = 0.f;
-        bool occl = false;
-        if (need) {
-          dvw = l2_exact<kVec4>(xv, x + uint64_t(key_id(wk)) * d, d);
-          occl = v_dist >= dvw;
-        }
-        const unsigned m_valid = __ballot_sync(0xffffffffu, valid);
-        const unsigned m_need = __ballot_sync(0xffffffffu, need);
-        const unsigned m_occ = __ballot_sync(0xffffffffu, occl);
-        if (m_occ) {
-          const int first = __ffs(m_occ) - 1;
-          const unsigned below = (1u << first) - 1u;  // lanes before occluder
-          if (lane == 0) {
-            checks += __popc(m_need & below) + 1;
-            skips += __popc(m_valid & ~m_need & below);
-          }
-          if (need && uint32_t(lane) <= uint32_t(first)) T[k] = 1;
-          w_id = key_id(__shfl_sync(0xffffffffu, wk, first));
-          w_dist = __shfl_sync(0xffffffffu, dvw, first);
-          any_need = true;
-          keep = false;
-          break;
-        }
-        if (lane == 0) {
-          checks += __popc(m_need);
-          skips += __popc(m_valid & ~m_need);
-        }
-        if (need) T[k] = 1;
-        any_need |= (m_need != 0);
-      }
-      if (lane == 0) {
-        if (any_need) T[i] = 1;
-        if (keep) {
-          L[nk] = vk;
-          pend_src[base + i] = kNone;
-        } else {
-          ++removed;
-          pend_src[base + i] = w_id;
-          pend_key[base + i] = make_key(w_dist, v_id, 1u);
-          atomicAdd(&bcnt[w_id], 1ull);
-        }
-      }
-      if (keep) ++nk;
-      __syncwarp();
-    }
-    // survivors are flagged old (builder.cpp:68)
-    for (uint32_t k = lane; k < nk; k += 32) L[k] &= ~1ull;
-    uint32_t t = 0;
-    for (uint32_t j = lane; j < U; j += 32) t += T[j];
-    touched += t;
-    if (lane == 0) post_cnt[u] = nk;
-    __syncwarp();
-  }
-  warp_add_counter(&ctr[kRemoved], removed);
-  warp_add_counter(&ctr[kPairChecks], checks);
-  warp_add_counter(&ctr[kFlagSkips], skips);
-  warp_add_counter(&ctr[kTouched], touched);
-}
+// The distance stage (scan_vertex, builder.cpp:41-69) lives in scan.cu.
 
 // Scatter emitted redirects into per-source buckets.
 __global__ void k_pend_scatter(uint64_t span, const uint32_t* __restrict__ pend_src,
@@ -566,7 +474,8 @@ void rebuild_and_swap(rnndg_ctx* c, const uint8_t* active, const uint32_t* post_
 void ensure_scratch(rnndg_ctx* c) {
   const uint64_t n = c->n, span = c->span ? c->span : 1;
   c->active.ensure(n);
-  c->act_list.ensure(n);
+  c->act_list.ensure(2 * n);
+  c->work.ensure(2);
   c->post_cnt.ensure(n + 1);
   c->cnt_b.ensure(n + 1);
   c->seg_end.ensure(n);
@@ -578,6 +487,8 @@ void ensure_scratch(rnndg_ctx* c) {
   c->pend_src.ensure(span);
   c->pend_key.ensure(span);
   c->touch.ensure(span);
+  c->kpos_g.ensure(span);
+  c->kpos2_g.ensure(span);
   c->bkey.ensure(span);
   c->bflag.ensure(span);
 }
@@ -638,15 +549,9 @@ void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_s
                c->key.p, c->active.p, c->seg_end.p, c->act_list.p, c->post_cnt.p, ctr);
   seg_sort_keys(c, c->key.p, c->key_s.p, c->span, n, c->off.p, c->seg_end.p);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
-  const unsigned scan_grid = unsigned(sm_count(c)) * 8;
-  if (c->d % 4 == 0)
-    RNNDG_LAUNCH(c, k_scan<true>, scan_grid, kBlock, 0, c->act_list.p, ctr, c->off.p,
-                 c->cnt.p, c->key_s.p, c->x, c->d, c->post_cnt.p, c->pend_src.p,
-                 c->pend_key.p, c->bcnt.p, c->touch.p, ctr);
-  else
-    RNNDG_LAUNCH(c, k_scan<false>, scan_grid, kBlock, 0, c->act_list.p, ctr, c->off.p,
-                 c->cnt.p, c->key_s.p, c->x, c->d, c->post_cnt.p, c->pend_src.p,
-                 c->pend_key.p, c->bcnt.p, c->touch.p, ctr);
+  // distance stage: push-formulated scan, one warp per vertex (scan.cu)
+  zero(c, c->work.p, 2);
+  launch_scan(c, c->work.p);
   RNNDG_CUDA(cudaEventRecord(c->ev[2], c->stream));
   scan_u64(c, c->bcnt.p, c->boff.p, n);
   RNNDG_LAUNCH(c, k_pend_scatter, grid_for(c->span, 256, 148 * 64), 256, 0, c->span,
@@ -669,6 +574,13 @@ void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_s
   if (t_scan) *t_scan += elapsed_ms(c->ev[1], c->ev[2]) * 1e-3;
   if (t_apply) *t_apply += elapsed_ms(c->ev[2], c->ev[3]) * 1e-3;
   if (touched) *touched += h[kTouched];
+  if (c->trace)
+    std::fprintf(stderr,
+                 "[rnndg] pass active=%llu large=%llu maxlen=%llu entries=%llu checks=%llu "
+                 "removed=%llu inserted=%llu touched=%llu sort=%.3fms scan=%.3fms apply=%.3fms\n",
+                 h[kActiveCount], h[kLargeCount], h[kMaxLen], h[kActiveEntries], h[kPairChecks],
+                 h[kRemoved], h[kInserted], h[kTouched], elapsed_ms(c->ev[0], c->ev[1]),
+                 elapsed_ms(c->ev[1], c->ev[2]), elapsed_ms(c->ev[2], c->ev[3]));
   if (active_entries) *active_entries += h[kActiveEntries];
 }
 

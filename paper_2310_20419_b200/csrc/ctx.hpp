@@ -72,6 +72,8 @@ enum Counter : int {
   kTouched,
   kActiveEntries,
   kActiveCount,
+  kLargeCount,
+  kMaxLen,
   kNumCounters
 };
 
@@ -80,6 +82,8 @@ enum Counter : int {
 struct rnndg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
+  cudaStream_t side = nullptr;  // concurrent long-list scan
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   uint64_t launches = 0;
 
@@ -105,6 +109,12 @@ struct rnndg_ctx {
   rnndg::DevBuf<unsigned long long> bcnt, bcur;
   rnndg::DevBuf<uint32_t> post_cnt;
   rnndg::DevBuf<unsigned long long> counters;
+  rnndg::DevBuf<unsigned int> work;
+  rnndg::DevBuf<uint32_t> kpos_g, kpos2_g;  // scan scratch for lists > kScanUcap
+  // chain-blocked copy of the store for the distance stage (scan.cu)
+  rnndg::DevBuf<float> xp;
+  const float* xp_src = nullptr;
+  uint32_t xp_stride = 0;
   rnndg::DevBuf<unsigned char> cub_tmp;
 
   // eval scratch
@@ -114,6 +124,7 @@ struct rnndg_ctx {
   rnndg::DevBuf<unsigned long long> qstat_dev;
 
   std::vector<rnndg_counts> pass_counts;
+  bool trace = false;  // RNNDG_TRACE=1: per-pass line on stderr
   // timing events
   cudaEvent_t ev[8] = {};
 };

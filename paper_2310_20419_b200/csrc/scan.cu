@@ -1,0 +1,452 @@
+// scan.cu -- the distance stage (scan_vertex, builder.cpp:41-69) on sm_100a.
+//
+// Formulation.  The reference walk is "pull": candidate v (ascending
+// (dist, id)) tests the kept list K in order and the first w with
+// v.dist >= d(v,w) removes it.  We run the equivalent "push": walk the sorted
+// list; the first still-alive candidate is kept (every earlier kept entry has
+// already been tested against it), then it is tested against every alive
+// candidate after it.  A pair (v, w) is evaluated iff w was kept before v and
+// v was still alive -- exactly the reference's pairs -- so pair_checks,
+// flag_skips (old/old pairs passed over), removed and each redirect
+// (w, v, d(v,w)) come out identical, with no speculative distance work.
+//
+// Mapping.  A push step's tests run 8 per warp at a time: one quad of lanes
+// per pair, one lane per fp32 chain.  The store is kept on the device in a
+// chain-blocked layout (k_chain_layout) so lane k reads chain k's next 8
+// elements with one 256-bit load (LDG.E.ENL2.256) and a quad reads a full
+// 128-byte line.  The chains are combined exactly as ((s0+s1)+(s2+s3)) and
+// the d % 4 tail is added in order (metric.hpp:15-24): bit-identical to
+// rnnd::l2_sq.  A vertex's rows are pulled into L2 with one bulk prefetch per
+// row (cp.async.bulk.prefetch.L2, UBLKPF) when its scan starts.
+//
+//   k_scan_push      one warp per vertex, lists <= kScanUcap: sorted keys and
+//                    the alive list live in shared memory
+//   k_scan_push_cta  one 1024-thread CTA per vertex for longer lists (hubs that
+//                    collect redirects); every push step is split over 32
+//                    warps.  Runs concurrently with k_scan_push on a second
+//                    stream.
+#include "common.cuh"
+#include "ctx.hpp"
+#include "scan.cuh"
+
+namespace rnndg {
+
+namespace {
+
+constexpr int kWarps = 8;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kBigThreads = 1024;
+constexpr int kBigWarps = kBigThreads / 32;
+
+// Chain-blocked row layout: element e < d4 = d - d % 4 lives at
+//   32 * (e / 32) + 8 * (e % 4) + (e % 32) / 4
+// i.e. per 32-element block, chain k's 8 elements are contiguous.  Padding
+// slots are +0 (adding (0-0)^2 = +0 to a chain sum is exact); the d % 4 tail
+// follows the blocks.  The row stride is a multiple of 8 floats (32 bytes).
+__global__ void k_chain_layout(const float* __restrict__ x, uint64_t n, uint32_t d,
+                               uint32_t stride, float* __restrict__ xp) {
+  const uint32_t d4 = d & ~3u;
+  const uint32_t nblk = (d4 + 31) / 32;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n * stride;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t r = i / stride;
+    const uint32_t s = uint32_t(i % stride);
+    float v = 0.f;
+    if (s < nblk * 32) {
+      const uint32_t b = s / 32, k = (s % 32) / 8, j = s % 8;
+      const uint32_t e = 32 * b + 4 * j + k;
+      if (e < d4) v = x[r * d + e];
+    } else {
+      const uint32_t t = s - nblk * 32;
+      if (t < d - d4) v = x[r * d + d4 + t];
+    }
+    xp[i] = v;
+  }
+}
+
+__device__ __forceinline__ void ld256(const float* p, float (&r)[8]) {
+  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                 "=f"(r[6]), "=f"(r[7])
+               : "l"(p));
+}
+
+__device__ __forceinline__ void prefetch_row_l2(const float* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void chain_step(const float (&va)[8], const float (&vb)[8], float& s) {
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const float t = __fsub_rn(va[i], vb[i]);
+    s = __fadd_rn(s, __fmul_rn(t, t));
+  }
+}
+
+// A quad computes d(a, b) on chain-blocked rows, lane k = chain k; the exact
+// total is returned in the quad's chain-0 lane.  All 32 lanes must call.
+// Loads run two blocks ahead of the arithmetic.
+__device__ __forceinline__ float quad_l2(const float* __restrict__ a, const float* __restrict__ b,
+                                         uint32_t k, uint32_t nblk, uint32_t ntail) {
+  float s = 0.f;
+  const float* pa = a + 8 * k;
+  const float* pb = b + 8 * k;
+  float a0[8], b0[8], a1[8], b1[8];
+  uint32_t blk = 0;
+  if (nblk >= 2) {
+    ld256(pa, a0);
+    ld256(pb, b0);
+    ld256(pa + 32, a1);
+    ld256(pb + 32, b1);
+    for (blk = 2; blk + 1 < nblk; blk += 2) {
+      chain_step(a0, b0, s);
+      ld256(pa + 32 * blk, a0);
+      ld256(pb + 32 * blk, b0);
+      chain_step(a1, b1, s);
+      ld256(pa + 32 * (blk + 1), a1);
+      ld256(pb + 32 * (blk + 1), b1);
+    }
+    chain_step(a0, b0, s);
+    chain_step(a1, b1, s);
+  }
+  for (; blk < nblk; ++blk) {
+    ld256(pa + 32 * blk, a0);
+    ld256(pb + 32 * blk, b0);
+    chain_step(a0, b0, s);
+  }
+  const float s_next = __shfl_down_sync(0xffffffffu, s, 1);
+  const float pair = __fadd_rn(s, s_next);                    // s0+s1 | s2+s3
+  const float pair2 = __shfl_down_sync(0xffffffffu, pair, 2);
+  float sum = __fadd_rn(pair, pair2);                         // chain-0 lane
+  if (ntail && k == 0) {
+    const float* ta = a + 32 * nblk;
+    const float* tb = b + 32 * nblk;
+    for (uint32_t t = 0; t < ntail; ++t) {
+      const float df = __fsub_rn(__ldg(ta + t), __ldg(tb + t));
+      sum = __fadd_rn(sum, __fmul_rn(df, df));
+    }
+  }
+  return sum;
+}
+
+struct Row {
+  const float* xp;
+  uint32_t stride, nblk, ntail;
+  __device__ const float* operator()(uint64_t key) const {
+    return xp + uint64_t(key_id(key)) * stride;
+  }
+};
+
+// One push round: the lanes' candidates (valid, key vk at list position q)
+// against the kept entry wk.  Returns whether this lane's candidate is removed
+// (and the occluding distance).  Accumulates the reference counters in lane 0
+// and marks touched list positions.
+__device__ __forceinline__ bool push_round(const Row& row, bool valid, uint32_t q, uint64_t vk,
+                                           uint64_t wk, uint32_t p, const float* xw, uint8_t* T,
+                                           float& dvw, unsigned long long& checks,
+                                           unsigned long long& skips) {
+  const uint32_t lane = lane_id();
+  const uint32_t quad = lane >> 2, chain = lane & 3;
+  const bool need = valid && (key_fresh(wk) || key_fresh(vk));  // builder.cpp:53-56
+  const unsigned m_valid = __ballot_sync(0xffffffffu, valid);
+  const unsigned m_need = __ballot_sync(0xffffffffu, need);
+  const uint32_t n_need = __popc(m_need);
+  if (lane == 0) {
+    skips += __popc(m_valid & ~m_need);
+    checks += n_need;
+  }
+  const uint32_t my_rank = __popc(m_need & ((1u << lane) - 1u));
+  const uint32_t first = __ffs(m_need) - 1;
+  bool gone = false;
+  for (uint32_t r0 = 0; r0 < n_need; r0 += 8) {
+    // quad j evaluates the (r0 + j)-th needed candidate of the round; quads
+    // without a task repeat the first one (keeps the shuffles uniform)
+    const uint32_t src = __fns(m_need, 0, int(r0 + quad + 1));
+    const bool has = src < 32u;
+    const uint32_t s = has ? src : first;
+    const uint32_t qs = __shfl_sync(0xffffffffu, q, s);
+    const uint64_t vks = __shfl_sync(0xffffffffu, vk, s);
+    const float dist = quad_l2(row(vks), xw, chain, row.nblk, row.ntail);
+    if (has && chain == 0) {
+      T[qs] = 1;
+      T[p] = 1;
+    }
+    const bool mine = need && my_rank >= r0 && my_rank < r0 + 8;
+    const float dq = __shfl_sync(0xffffffffu, dist, mine ? 4 * (my_rank - r0) : 0);
+    if (mine) {
+      dvw = dq;
+      gone = key_dist(vk) >= dq;
+    }
+  }
+  return gone;
+}
+
+__device__ __forceinline__ void emit_redirect(uint64_t base, uint32_t q, uint64_t vk, uint64_t wk,
+                                              float dvw, uint32_t* pend_src, uint64_t* pend_key,
+                                              unsigned long long* bcnt) {
+  const uint32_t w_id = key_id(wk);
+  pend_src[base + q] = w_id;
+  pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
+  atomicAdd(&bcnt[w_id], 1ull);
+}
+
+struct ScanArgs {
+  const uint32_t* act_list;
+  uint64_t n;
+  const unsigned long long* ctr_in;
+  unsigned int* work;
+  const uint64_t* off;
+  const uint32_t* cnt;
+  uint64_t* keys;
+  Row row;
+  uint32_t* alive_g;
+  uint32_t* alive2_g;
+  uint8_t* touch;
+  uint32_t* post_cnt;
+  uint32_t* pend_src;
+  uint64_t* pend_key;
+  unsigned long long* bcnt;
+  unsigned long long* ctr;
+};
+
+__device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned long long removed,
+                                               unsigned long long checks,
+                                               unsigned long long skips,
+                                               unsigned long long touched) {
+  for (int o = 16; o; o >>= 1) {
+    touched += __shfl_xor_sync(0xffffffffu, touched, o);
+    removed += __shfl_xor_sync(0xffffffffu, removed, o);
+    checks += __shfl_xor_sync(0xffffffffu, checks, o);
+    skips += __shfl_xor_sync(0xffffffffu, skips, o);
+  }
+  if (lane_id() == 0) {
+    if (touched) atomicAdd(&ctr[kTouched], touched);
+    if (removed) atomicAdd(&ctr[kRemoved], removed);
+    if (checks) atomicAdd(&ctr[kPairChecks], checks);
+    if (skips) atomicAdd(&ctr[kFlagSkips], skips);
+  }
+}
+
+// ---------------------------------------------------------------- small
+__global__ void __launch_bounds__(kThreads) k_scan_push(ScanArgs g) {
+  __shared__ uint64_t keys_sh[kWarps][kScanUcap];
+  __shared__ uint32_t alive_sh[kWarps][kScanUcap];
+  const uint32_t lane = lane_id();
+  const uint32_t wib = threadIdx.x >> 5;
+  const unsigned below = (1u << lane) - 1u;
+  const uint32_t nact = uint32_t(g.ctr_in[kActiveCount]);
+  const Row row = g.row;  // local copy (no generic pointers into param space)
+  const uint32_t row_bytes = row.stride * 4u;
+  uint64_t* K = keys_sh[wib];
+  uint32_t* A = alive_sh[wib];
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
+
+  for (;;) {
+    uint32_t a = 0;
+    if (lane == 0) a = atomicAdd(g.work, 1u);
+    a = __shfl_sync(0xffffffffu, a, 0);
+    if (a >= nact) break;
+    const uint32_t u = g.act_list[a];
+    const uint64_t base = g.off[u];
+    const uint32_t U = g.cnt[u];
+    uint64_t* L = g.keys + base;
+    uint8_t* T = g.touch + base;
+    for (uint32_t j = lane; j < U; j += 32) {
+      const uint64_t k = L[j];
+      K[j] = k;
+      A[j] = j;
+      prefetch_row_l2(row(k), row_bytes);
+    }
+    __syncwarp();
+    uint32_t na = U, nk = 0;
+    while (na) {
+      // the first alive candidate is kept: every earlier kept entry has
+      // already been tested against it
+      const uint32_t p = A[0];
+      const uint64_t wk = K[p];
+      const float* xw = row(wk);
+      if (lane == 0) L[nk] = wk & ~1ull;  // flagged old (builder.cpp:68)
+      ++nk;
+      uint32_t nn = 0;  // survivors, compacted into A[0 ..) in order
+      for (uint32_t g0 = 1; g0 < na; g0 += 32) {
+        const uint32_t gi = g0 + lane;
+        const bool valid = gi < na;
+        const uint32_t q = valid ? A[gi] : 0u;
+        const uint64_t vk = valid ? K[q] : 0ull;
+        float dvw = 0.f;
+        const bool gone = push_round(row, valid, q, vk, wk, p, xw, T, dvw, checks, skips);
+        if (gone) {
+          ++removed;
+          emit_redirect(base, q, vk, wk, dvw, g.pend_src, g.pend_key, g.bcnt);
+        }
+        const bool stay = valid && !gone;
+        const unsigned m_stay = __ballot_sync(0xffffffffu, stay);
+        __syncwarp();
+        if (stay) A[nn + __popc(m_stay & below)] = q;
+        nn += __popc(m_stay);
+        __syncwarp();
+      }
+      na = nn;
+    }
+    if (lane == 0) g.post_cnt[u] = nk;
+    for (uint32_t j = lane; j < U; j += 32) touched += T[j];
+    __syncwarp();
+  }
+  flush_counters(g.ctr, removed, checks, skips, touched);
+}
+
+// ------------------------------------------------------------------ big
+// One CTA per long list.  Each push step: thread 0's view of A[0] is the kept
+// entry; the alive candidates A[1 .. na) are split into contiguous ranges,
+// one per warp; survivors are compacted per warp into A2 and then gathered,
+// in order, back into A.
+__global__ void __launch_bounds__(kBigThreads) k_scan_push_cta(ScanArgs g) {
+  __shared__ uint32_t wcount[kBigWarps];
+  __shared__ uint32_t wstart[kBigWarps];
+  __shared__ uint32_t s_a, s_na;
+  const uint32_t lane = lane_id();
+  const uint32_t wid = threadIdx.x >> 5;
+  const unsigned below = (1u << lane) - 1u;
+  const uint32_t nlarge = uint32_t(g.ctr_in[kLargeCount]);
+  const Row row = g.row;
+  const uint32_t row_bytes = row.stride * 4u;
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
+
+  for (;;) {
+    if (threadIdx.x == 0) s_a = atomicAdd(g.work + 1, 1u);
+    __syncthreads();
+    const uint32_t a = s_a;
+    if (a >= nlarge) break;
+    const uint32_t u = g.act_list[g.n + a];
+    const uint64_t base = g.off[u];
+    const uint32_t U = g.cnt[u];
+    uint64_t* L = g.keys + base;
+    uint8_t* T = g.touch + base;
+    uint32_t* A = g.alive_g + base;
+    uint32_t* A2 = g.alive2_g + base;
+    for (uint32_t j = threadIdx.x; j < U; j += kBigThreads) {
+      A[j] = j;
+      prefetch_row_l2(row(L[j]), row_bytes);
+    }
+    if (threadIdx.x == 0) s_na = U;
+    __syncthreads();
+    uint32_t nk = 0;
+    // The kept entry of a step is written to L[nk] in place; L[q] for alive
+    // q > p is never overwritten (nk <= p), so candidates read keys from L.
+    for (;;) {
+      const uint32_t na = s_na;
+      if (na == 0) break;
+      const uint32_t p = A[0];
+      const uint64_t wk = L[p];
+      const float* xw = row(wk);
+      __syncthreads();  // everyone has read A[0] and L[p]
+      if (threadIdx.x == 0) L[nk] = wk & ~1ull;
+      ++nk;
+      // warp w takes candidates [1 + w*span, 1 + (w+1)*span)
+      const uint32_t ncand = na - 1;
+      const uint32_t span = ((ncand + kBigWarps - 1) / kBigWarps + 31) & ~31u;
+      const uint32_t lo = 1 + wid * span;
+      const uint32_t hi = lo + span < na ? lo + span : na;
+      uint32_t nn = 0;
+      for (uint32_t g0 = lo; g0 < hi; g0 += 32) {
+        const uint32_t gi = g0 + lane;
+        const bool valid = gi < hi;
+        const uint32_t q = valid ? A[gi] : 0u;
+        const uint64_t vk = valid ? L[q] : 0ull;
+        float dvw = 0.f;
+        const bool gone = push_round(row, valid, q, vk, wk, p, xw, T, dvw, checks, skips);
+        if (gone) {
+          ++removed;
+          emit_redirect(base, q, vk, wk, dvw, g.pend_src, g.pend_key, g.bcnt);
+        }
+        const bool stay = valid && !gone;
+        const unsigned m_stay = __ballot_sync(0xffffffffu, stay);
+        if (stay) A2[lo - 1 + nn + __popc(m_stay & below)] = q;
+        nn += __popc(m_stay);
+      }
+      if (lane == 0) wcount[wid] = lo < na ? nn : 0u;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (int w = 0; w < kBigWarps; ++w) {
+          wstart[w] = t;
+          t += wcount[w];
+        }
+        s_na = t;
+      }
+      __syncthreads();
+      if (lo < na) {
+        const uint32_t cnt_w = wcount[wid], dst = wstart[wid];
+        for (uint32_t j = lane; j < cnt_w; j += 32) A[dst + j] = A2[lo - 1 + j];
+      }
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) g.post_cnt[u] = nk;
+    for (uint32_t j = threadIdx.x; j < U; j += kBigThreads) touched += T[j];
+    __syncthreads();
+  }
+  flush_counters(g.ctr, removed, checks, skips, touched);
+}
+
+}  // namespace
+
+ScanConfig scan_config(rnndg_ctx* c) {
+  ScanConfig cfg{};
+  const uint32_t d = c->d;
+  const uint32_t d4 = d & ~3u;
+  cfg.nblk = (d4 + 31) / 32;
+  cfg.ntail = d - d4;
+  cfg.stride = cfg.nblk * 32 + (cfg.ntail ? 8 : 0);
+  return cfg;
+}
+
+void prepare_chain_layout(rnndg_ctx* c) {
+  const ScanConfig cfg = scan_config(c);
+  if (c->xp_src == c->x && c->xp_stride == cfg.stride && c->xp.p) return;
+  const uint64_t total = c->n * cfg.stride;
+  c->xp.ensure(total);
+  const uint64_t blocks = (total + 255) / 256;
+  const unsigned grid = unsigned(blocks < (1u << 20) ? blocks : (1u << 20));
+  RNNDG_LAUNCH(c, k_chain_layout, grid, 256, 0, c->x, c->n, c->d, cfg.stride, c->xp.p);
+  c->xp_src = c->x;
+  c->xp_stride = cfg.stride;
+}
+
+// Launches both scan kernels; the long-list kernel runs on the side stream
+// and is joined back before returning.  work[0] / work[1] are the queues.
+void launch_scan(rnndg_ctx* c, unsigned int* work) {
+  const ScanConfig cfg = scan_config(c);
+  prepare_chain_layout(c);
+  ScanArgs a{};
+  a.act_list = c->act_list.p;
+  a.n = c->n;
+  a.ctr_in = c->counters.p;
+  a.work = work;
+  a.off = c->off.p;
+  a.cnt = c->cnt.p;
+  a.keys = c->key_s.p;
+  a.row = Row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail};
+  a.alive_g = c->kpos_g.p;
+  a.alive2_g = c->kpos2_g.p;
+  a.touch = c->touch.p;
+  a.post_cnt = c->post_cnt.p;
+  a.pend_src = c->pend_src.p;
+  a.pend_key = c->pend_key.p;
+  a.bcnt = c->bcnt.p;
+  a.ctr = c->counters.p;
+  static thread_local int per_sm = 0;
+  if (!per_sm)
+    RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_push, kThreads, 0));
+  const unsigned grid = unsigned(sm_count(c)) * unsigned(per_sm > 0 ? per_sm : 1);
+  // fork: side stream waits for everything issued so far on the main stream
+  RNNDG_CUDA(cudaEventRecord(c->ev_fork, c->stream));
+  RNNDG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
+  k_scan_push_cta<<<unsigned(sm_count(c)) / 4, kBigThreads, 0, c->side>>>(a);
+  ++c->launches;
+  RNNDG_CUDA(cudaGetLastError());
+  RNNDG_LAUNCH(c, k_scan_push, grid, kThreads, 0, a);
+  RNNDG_CUDA(cudaEventRecord(c->ev_join, c->side));
+  RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+}
+
+}  // namespace rnndg
