@@ -245,7 +245,8 @@ int rnndg_build(rnndg_ctx* c, uint32_t S, uint32_t R, uint32_t T1, uint32_t T2,
         progress(t1, T1, &outer, ms * 1e-3, user);
       }
     }
-    op_sort_lists(c);  // builder.cpp:283-285
+    // builder.cpp:283-285 sorts every list nearest-first: the device lists
+    // are always sorted (build.cu invariant), so there is nothing left to do
     RNNDG_CUDA(cudaEventRecord(c->ev[5], c->stream));
     RNNDG_CUDA(cudaEventSynchronize(c->ev[5]));
     float ms = 0.f;
@@ -339,6 +340,11 @@ int rnndg_set_graph(rnndg_ctx* c, uint64_t n, const uint64_t* offsets, const uin
     c->span = m;
     c->has_graph = true;
     c->has_distances = dists != nullptr;
+    // graphs with cached distances keep every list sorted by (dist, id)
+    // (build.cu invariant); a graph loaded without distances keeps its stored
+    // order, which select_nearest then uses (graph.cpp:65-74)
+    if (c->has_distances) op_sort_lists(c);
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

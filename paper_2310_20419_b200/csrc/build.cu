@@ -1,33 +1,41 @@
-// build.cu -- the RNN-Descent update loop on sm_100a.
+// build.cu -- the RNN-Descent update loop on sm_100a (everything except the
+// distance stage, which lives in scan.cu).
 //
 // Reference: /root/reference/proj/src/builder.cpp (update_parallel :88-139,
-// scan_vertex :41-69, add_reverse_edges :222-251, out_prune :141-150,
-// in_prune :152-192, final sort :283-285) and graph.cpp random_init :47-63.
+// add_reverse_edges :222-251, out_prune :141-150, in_prune :152-192, final
+// sort :283-285) and graph.cpp random_init :47-63.
 //
-// State is a set of entries per vertex; every step below is order-canonical
-// (sorted scans, set-union appends, sort-based prunes), so the device graph is
-// identical, entry for entry, to rnnd::build with threads > 1.
+// Invariant: every list of the current graph is sorted ascending by key
+// (= `nearer`, dist then id).  The state is a set per vertex, so ordering is
+// free to choose; keeping it sorted means
+//   * the scan needs no per-pass sort (builder.cpp:48 is a no-op),
+//   * out_prune is a truncation, the final sort is a no-op,
+//   * append-if-absent is a binary search: every cached distance is the exact
+//     l2 of its two endpoints (init, redirect and reverse all store
+//     l2_sq(row a, row b), which is bit-symmetric), so a proposal (w, v, d)
+//     is already in w's list iff an entry with the same (dist, id) exists.
 //
-// One update pass (all on one stream, no host round trip except the size of
-// the rebuilt CSR):
-//   k_mark_active    vertices with >= 1 fresh entry; inactive ones are exact
-//                    no-ops contributing U(U-1)/2 flag skips
-//   segmented sort   active lists ascending (dist, id)  (builder.cpp:48)
-//   k_scan           occlusion scan + redirect emission (builder.cpp:50-68)
-//   bucket pending   by redirect source (count fused into k_scan, scan,
-//                    k_scatter)
-//   k_apply_count    dedupe + append-if-absent decisions (builder.cpp:117-136)
-//   scan + k_rebuild new CSR
+// One update pass (one stream, one host sync for the rebuilt CSR size):
+//   k_mark_active       active = >= 1 fresh entry; inactive vertices are exact
+//                       no-ops contributing U(U-1)/2 flag skips (builder.cpp:53-56)
+//   locality order      3-hop min-id label over the graph, radix sort, select
+//                       (processing order only; results are order-independent)
+//   scan (scan.cu)      push-formulated occlusion scan, redirects bucketed by w
+//   bucket sort         CUB segmented sort of each source's proposals
+//   k_apply_count       dedupe (adjacent equal keys) + binary-search membership
+//   k_merge             merge post-scan list and new entries into the next CSR
 #define CCCL_IGNORE_DEPRECATED_API
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
+#include <cub/device/device_select.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
+
+#include <cstdio>
 
 #include "common.cuh"
 #include "ctx.hpp"
 #include "scan.cuh"
-
-#include <cstdio>
 
 namespace rnndg {
 
@@ -35,6 +43,7 @@ namespace {
 
 constexpr int kWarpsPerBlock = 8;
 constexpr int kBlock = 32 * kWarpsPerBlock;
+constexpr int kLabelRounds = 3;
 
 struct ToU64 {
   __host__ __device__ uint64_t operator()(uint32_t v) const { return v; }
@@ -52,6 +61,24 @@ __device__ __forceinline__ void warp_add_counter(unsigned long long* ctr,
   if (lane_id() == 0 && v) atomicAdd(ctr, v);
 }
 
+// first index in [0, m) with a[i] >= key
+__device__ __forceinline__ uint32_t lower_bound(const uint64_t* a, uint32_t m, uint64_t key) {
+  uint32_t lo = 0, hi = m;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < key)
+      lo = mid + 1;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+#define WARP_LOOP(var, count)                                                      \
+  const uint64_t warp_ = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; \
+  const uint64_t nwarps_ = (uint64_t(gridDim.x) * blockDim.x) >> 5;             \
+  for (uint64_t var = warp_; var < (count); var += nwarps_)
+
 // ------------------------------------------------------------- random init
 // graph.cpp:47-63.  One warp per vertex: lane 0 runs Floyd's sampling
 // (rng.hpp:46-72; the emitted-set test is a linear scan, which is exactly the
@@ -61,10 +88,8 @@ template <bool kVec4>
 __global__ void k_random_init(uint64_t n, uint32_t S, uint64_t seed,
                               const float* __restrict__ x, uint32_t d,
                               uint64_t* __restrict__ key) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t lane = lane_id();
-  for (uint64_t u = warp; u < n; u += nwarps) {
+  WARP_LOOP(u, n) {
     uint64_t* out = key + u * S;
     if (lane == 0) {
       SplitMix64 rng(mix_seed(seed, u));
@@ -92,68 +117,93 @@ __global__ void k_random_init(uint64_t n, uint32_t S, uint64_t seed,
   }
 }
 
-__global__ void k_fill_offsets(uint64_t n, uint32_t S, uint64_t* off,
-                               uint32_t* cnt) {
+__global__ void k_fill_offsets(uint64_t n, uint32_t S, uint64_t* off, uint32_t* cnt) {
   uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (u <= n) off[u] = u * S;
   if (u < n) cnt[u] = S;
 }
 
 // ------------------------------------------------------------ mark active
-// A vertex with no fresh entry is an exact no-op of scan_vertex: every pair
-// is old/old, nothing is removed, the list keeps its set of entries
-// (builder.cpp:53-56) and it contributes U(U-1)/2 flag skips.
+// Long lists (> kScanUcap) are queued to act_list[n ..) for the CTA scan;
+// short active lists are selected later in locality order.
 __global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
                               const uint32_t* __restrict__ cnt,
                               const uint64_t* __restrict__ key,
                               uint8_t* __restrict__ active,
-                              uint64_t* __restrict__ seg_end,
                               uint32_t* __restrict__ act_list,
                               uint32_t* __restrict__ post_cnt,
                               unsigned long long* __restrict__ ctr) {
-  uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  unsigned long long skips = 0, aentries = 0;
-  bool act = false;
+  const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  unsigned long long skips = 0, aentries = 0, nact = 0;
+  bool large = false;
   if (u < n) {
     const uint64_t b = off[u];
     const uint32_t U = cnt[u];
+    bool act = false;
     for (uint32_t j = 0; j < U; ++j)
       if (key_fresh(key[b + j])) {
         act = true;
         break;
       }
-    active[u] = act ? 1 : 0;
-    seg_end[u] = act ? b + U : b;
+    uint8_t flag = 0;
     if (act) {
       aentries = U;
+      nact = 1;
+      large = U > kScanUcap;
+      flag = large ? 2 : 1;
       atomicMax(&ctr[kMaxLen], (unsigned long long)U);
     } else {
       post_cnt[u] = U;
       skips = (unsigned long long)U * (U ? U - 1 : 0) / 2;
     }
+    active[u] = flag;
   }
-  // warp-aggregated append of active ids: lists that fit the CTA scan's
-  // shared-memory arrays go to act_list[0..), longer ones to act_list[n..)
-  const bool small = act && cnt[u < n ? u : 0] <= kScanUcap;
-  const bool large = act && !small;
-  const unsigned ms = __ballot_sync(0xffffffffu, small);
   const unsigned ml = __ballot_sync(0xffffffffu, large);
-  uint32_t bs = 0, bl = 0;
-  if (lane_id() == 0) {
-    if (ms) bs = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kActiveCount]), __popc(ms));
-    if (ml) bl = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLargeCount]), __popc(ml));
-  }
-  bs = __shfl_sync(0xffffffffu, bs, 0);
+  uint32_t bl = 0;
+  if (lane_id() == 0 && ml)
+    bl = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLargeCount]), __popc(ml));
   bl = __shfl_sync(0xffffffffu, bl, 0);
-  const unsigned below = (1u << lane_id()) - 1;
-  if (small) act_list[bs + __popc(ms & below)] = uint32_t(u);
-  if (large) act_list[n + bl + __popc(ml & below)] = uint32_t(u);
+  if (large) act_list[n + bl + __popc(ml & ((1u << lane_id()) - 1))] = uint32_t(u);
   warp_add_counter(&ctr[kFlagSkips], skips);
   warp_add_counter(&ctr[kActiveEntries], aentries);
+  warp_add_counter(&ctr[kActiveCount], nact);
 }
 
-// The distance stage (scan_vertex, builder.cpp:41-69) lives in scan.cu.
+// ---------------------------------------------------------- locality order
+// label(u) <- min(label(u), label of every out-neighbour), kLabelRounds times:
+// the minimum id within 3 hops.  Vertices of one neighbourhood share a label,
+// so scanning in (label, id) order keeps concurrently scanned lists
+// overlapping and their rows resident in L2.  Results do not depend on it.
+__global__ void k_label_step(uint64_t n, const uint64_t* __restrict__ off,
+                             const uint32_t* __restrict__ cnt,
+                             const uint64_t* __restrict__ key,
+                             const uint32_t* __restrict__ lab_in,
+                             uint32_t* __restrict__ lab_out) {
+  const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u >= n) return;
+  uint32_t m = lab_in ? lab_in[u] : uint32_t(u);
+  const uint64_t b = off[u];
+  const uint32_t U = cnt[u];
+  for (uint32_t j = 0; j < U; ++j) {
+    const uint32_t v = key_id(key[b + j]);
+    const uint32_t l = lab_in ? lab_in[v] : v;
+    m = l < m ? l : m;
+  }
+  lab_out[u] = m;
+}
 
+__global__ void k_order_keys(uint64_t n, const uint32_t* __restrict__ label,
+                             uint64_t* __restrict__ okey) {
+  const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u < n) okey[u] = (uint64_t(label[u]) << 32) | u;
+}
+
+struct IsShortActive {
+  const uint8_t* active;
+  __host__ __device__ bool operator()(uint64_t k) const { return active[uint32_t(k)] == 1; }
+};
+
+// ------------------------------------------------------------------ apply
 // Scatter emitted redirects into per-source buckets.
 __global__ void k_pend_scatter(uint64_t span, const uint32_t* __restrict__ pend_src,
                                const uint64_t* __restrict__ pend_key,
@@ -170,74 +220,96 @@ __global__ void k_pend_scatter(uint64_t span, const uint32_t* __restrict__ pend_
 }
 
 // Append-if-absent decisions (builder.cpp:117-136 / :236-243), one warp per
-// vertex.  A bucket entry is dropped when its id is already in the vertex's
-// post-scan list or (dedupe) when an earlier bucket entry carries the same
-// id: duplicate redirects carry bit-identical distances (l2 is evaluated as
-// l2(row v, row w) everywhere), so keeping any one of them equals the
-// reference's sort + unique.  new_cnt = post count + insertions.
+// vertex, on a bucket sorted by key.  A proposal is dropped when it equals the
+// previous proposal (duplicate redirects carry bit-identical keys, so keeping
+// one equals the reference's sort + unique) or when the post list already
+// holds the same (dist, id).  brank = exclusive rank among kept proposals.
 __global__ void __launch_bounds__(kBlock)
     k_apply_count(uint64_t n, const uint64_t* __restrict__ off,
-                  const uint8_t* __restrict__ active,
-                  const uint64_t* __restrict__ key_a,
-                  const uint64_t* __restrict__ key_s,
-                  const uint32_t* __restrict__ post_cnt,
-                  const uint64_t* __restrict__ boff,
-                  const uint64_t* __restrict__ bkey, uint8_t* __restrict__ bflag,
-                  uint32_t* __restrict__ new_cnt, int dedupe,
-                  unsigned long long* __restrict__ ctr) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+                  const uint64_t* __restrict__ key, const uint32_t* __restrict__ post_cnt,
+                  const uint64_t* __restrict__ boff, const uint64_t* __restrict__ bkey,
+                  uint8_t* __restrict__ bflag, uint32_t* __restrict__ brank,
+                  uint32_t* __restrict__ new_cnt, unsigned long long* __restrict__ ctr,
+                  int count_inserted) {
   const uint32_t lane = lane_id();
   unsigned long long inserted = 0;
-  for (uint64_t u = warp; u < n; u += nwarps) {
+  WARP_LOOP(u, n) {
     const uint64_t b0 = boff[u], b1 = boff[u + 1];
     const uint32_t pc = post_cnt[u];
     if (b0 == b1) {
       if (lane == 0) new_cnt[u] = pc;
       continue;
     }
-    const uint64_t* P = (active && active[u] ? key_s : key_a) + off[u];
+    const uint64_t* P = key + off[u];
     uint32_t ins = 0;
     for (uint64_t xb = b0; xb < b1; xb += 32) {
       const uint64_t xi = xb + lane;
+      bool keep = false;
       if (xi < b1) {
-        const uint32_t id = key_id(bkey[xi]);
-        bool drop = false;
-        if (dedupe)
-          for (uint64_t y = b0; y < xi && !drop; ++y) drop = key_id(bkey[y]) == id;
-        for (uint32_t j = 0; j < pc && !drop; ++j) {
-          const uint64_t pk = P[j];
-          drop = pk != kTomb && key_id(pk) == id;
+        const uint64_t k = bkey[xi];
+        const bool dup = xi > b0 && bkey[xi - 1] == k;
+        bool present = false;
+        if (!dup) {
+          const uint32_t pos = lower_bound(P, pc, k & ~1ull);
+          present = pos < pc && (P[pos] >> 1) == (k >> 1);
         }
-        bflag[xi] = drop ? 1 : 0;
-        ins += drop ? 0 : 1;
+        keep = !dup && !present;
+        bflag[xi] = keep ? 0 : 1;
       }
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      if (xi < b1) brank[xi] = ins + __popc(m & ((1u << lane) - 1));
+      ins += __popc(m);
     }
-    ins = uint32_t(warp_sum(ins));
     if (lane == 0) new_cnt[u] = pc + ins;
     inserted += lane == 0 ? ins : 0;
   }
-  if (lane == 0 && inserted) atomicAdd(&ctr[kInserted], inserted);
+  if (lane == 0 && inserted && count_inserted) atomicAdd(&ctr[kInserted], inserted);
 }
 
-// Write the next CSR: each vertex's post list (tombstones dropped) followed
-// by its undropped bucket entries.  One warp per vertex, ballot compaction.
+// Next CSR = merge(post list, kept proposals), both sorted by key, so the
+// output stays sorted.  Element positions come from binary searches.
 __global__ void __launch_bounds__(kBlock)
-    k_rebuild(uint64_t n, const uint64_t* __restrict__ off,
-              const uint8_t* __restrict__ active,
-              const uint64_t* __restrict__ key_a,
-              const uint64_t* __restrict__ key_s,
-              const uint32_t* __restrict__ post_cnt,
-              const uint64_t* __restrict__ boff,
-              const uint64_t* __restrict__ bkey,
-              const uint8_t* __restrict__ bflag,
-              const uint64_t* __restrict__ off_b, uint64_t* __restrict__ key_b) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+    k_merge(uint64_t n, const uint64_t* __restrict__ off, const uint64_t* __restrict__ key,
+            const uint32_t* __restrict__ post_cnt, const uint64_t* __restrict__ boff,
+            const uint64_t* __restrict__ bkey, const uint8_t* __restrict__ bflag,
+            const uint32_t* __restrict__ brank, const uint64_t* __restrict__ off_b,
+            uint64_t* __restrict__ key_b) {
   const uint32_t lane = lane_id();
-  for (uint64_t u = warp; u < n; u += nwarps) {
-    const uint64_t* P = (active && active[u] ? key_s : key_a) + off[u];
+  WARP_LOOP(u, n) {
+    const uint64_t* P = key + off[u];
     const uint32_t pc = post_cnt[u];
+    uint64_t* dst = key_b + off_b[u];
+    const uint64_t b0 = boff[u], b1 = boff[u + 1];
+    const uint32_t nb = uint32_t(b1 - b0);
+    const uint64_t* Bk = bkey + b0;
+    if (nb == 0) {
+      for (uint32_t j = lane; j < pc; j += 32) dst[j] = P[j];
+      continue;
+    }
+    const uint32_t ins = uint32_t(off_b[u + 1] - off_b[u]) - pc;
+    for (uint32_t j = lane; j < pc; j += 32) {
+      const uint64_t k = P[j];
+      const uint32_t lb = lower_bound(Bk, nb, k);
+      const uint32_t r = lb < nb ? brank[b0 + lb] : ins;
+      dst[j + r] = k;
+    }
+    for (uint32_t x = lane; x < nb; x += 32) {
+      if (bflag[b0 + x]) continue;
+      const uint64_t k = Bk[x];
+      dst[brank[b0 + x] + lower_bound(P, pc, k)] = k;
+    }
+  }
+}
+
+// Copy lists without tombstones (order, hence sortedness, is preserved).
+__global__ void __launch_bounds__(kBlock)
+    k_compact(uint64_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+              const uint64_t* __restrict__ key, const uint64_t* __restrict__ off_b,
+              uint64_t* __restrict__ key_b) {
+  const uint32_t lane = lane_id();
+  WARP_LOOP(u, n) {
+    const uint64_t* P = key + off[u];
+    const uint32_t pc = cnt[u];
     uint64_t* dst = key_b + off_b[u];
     uint32_t w = 0;
     for (uint32_t j0 = 0; j0 < pc; j0 += 32) {
@@ -248,16 +320,6 @@ __global__ void __launch_bounds__(kBlock)
       if (live) dst[w + __popc(m & ((1u << lane) - 1))] = k;
       w += __popc(m);
     }
-    if (boff) {
-      const uint64_t b0 = boff[u], b1 = boff[u + 1];
-      for (uint64_t xb = b0; xb < b1; xb += 32) {
-        const uint64_t xi = xb + lane;
-        const bool live = xi < b1 && !bflag[xi];
-        const unsigned m = __ballot_sync(0xffffffffu, live);
-        if (live) dst[w + __popc(m & ((1u << lane) - 1))] = bkey[xi];
-        w += __popc(m);
-      }
-    }
   }
 }
 
@@ -266,13 +328,10 @@ __global__ void __launch_bounds__(kBlock)
 // the same cached distance, flagged fresh, appended when absent.
 __global__ void __launch_bounds__(kBlock)
     k_count_targets(uint64_t n, const uint64_t* __restrict__ off,
-                    const uint32_t* __restrict__ cnt,
-                    const uint64_t* __restrict__ key,
+                    const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ key,
                     unsigned long long* __restrict__ bcnt) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t lane = lane_id();
-  for (uint64_t u = warp; u < n; u += nwarps) {
+  WARP_LOOP(u, n) {
     const uint64_t b = off[u];
     const uint32_t U = cnt[u];
     for (uint32_t j = lane; j < U; j += 32) atomicAdd(&bcnt[key_id(key[b + j])], 1ull);
@@ -283,16 +342,11 @@ __global__ void __launch_bounds__(kBlock)
 // (dist bits << 32 | source) with the edge slot as payload (in_prune).
 __global__ void __launch_bounds__(kBlock)
     k_scatter_targets(uint64_t n, const uint64_t* __restrict__ off,
-                      const uint32_t* __restrict__ cnt,
-                      const uint64_t* __restrict__ key,
-                      const uint64_t* __restrict__ boff,
-                      unsigned long long* __restrict__ bcur,
-                      uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpay,
-                      int mode) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+                      const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ key,
+                      const uint64_t* __restrict__ boff, unsigned long long* __restrict__ bcur,
+                      uint64_t* __restrict__ bkey, uint32_t* __restrict__ bpay, int mode) {
   const uint32_t lane = lane_id();
-  for (uint64_t u = warp; u < n; u += nwarps) {
+  WARP_LOOP(u, n) {
     const uint64_t b = off[u];
     const uint32_t U = cnt[u];
     for (uint32_t j = lane; j < U; j += 32) {
@@ -309,7 +363,8 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
-// segment ends for "sort only lists longer than R" (out_prune) or all lists
+// segment ends: [begin, begin + len) where len = cnt or bucket size, or empty
+// when the segment has <= R entries (R = 0: every non-empty segment)
 __global__ void k_seg_end(uint64_t n, const uint64_t* __restrict__ begin,
                           const uint32_t* __restrict__ cnt,
                           const uint64_t* __restrict__ boff, uint32_t R,
@@ -320,33 +375,20 @@ __global__ void k_seg_end(uint64_t n, const uint64_t* __restrict__ begin,
   seg_end[u] = begin[u] + (len > R ? len : 0);
 }
 
-// out_prune, builder.cpp:141-150: a list longer than R keeps its R nearest.
-__global__ void __launch_bounds__(kBlock)
-    k_out_take(uint64_t n, const uint64_t* __restrict__ off,
-               uint32_t* __restrict__ cnt, const uint64_t* __restrict__ key_s,
-               uint64_t* __restrict__ key, uint32_t R) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
-  const uint32_t lane = lane_id();
-  for (uint64_t u = warp; u < n; u += nwarps) {
-    if (cnt[u] <= R) continue;
-    const uint64_t b = off[u];
-    for (uint32_t j = lane; j < R; j += 32) key[b + j] = key_s[b + j];
-    __syncwarp();
-    if (lane == 0) cnt[u] = R;
-  }
+// out_prune, builder.cpp:141-150: a list longer than R keeps its R nearest;
+// lists are sorted, so that is a truncation.
+__global__ void k_out_trunc(uint64_t n, uint32_t* __restrict__ cnt, uint32_t R) {
+  uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u < n && cnt[u] > R) cnt[u] = R;
 }
 
 // in_prune, builder.cpp:162-176: in-edges of each target sorted by
 // (dist, source); ranks >= R are deleted from their source lists.
 __global__ void __launch_bounds__(kBlock)
     k_in_mark(uint64_t n, const uint64_t* __restrict__ boff,
-              const uint32_t* __restrict__ bpay_s, uint64_t* __restrict__ key,
-              uint32_t R) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+              const uint32_t* __restrict__ bpay_s, uint64_t* __restrict__ key, uint32_t R) {
   const uint32_t lane = lane_id();
-  for (uint64_t t = warp; t < n; t += nwarps) {
+  WARP_LOOP(t, n) {
     const uint64_t b0 = boff[t], b1 = boff[t + 1];
     if (b1 - b0 <= R) continue;
     for (uint64_t r = b0 + R + lane; r < b1; r += 32) key[bpay_s[r]] = kTomb;
@@ -354,13 +396,10 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 __global__ void __launch_bounds__(kBlock)
-    k_count_live(uint64_t n, const uint64_t* __restrict__ off,
-                 const uint32_t* __restrict__ cnt,
+    k_count_live(uint64_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ cnt,
                  const uint64_t* __restrict__ key, uint32_t* __restrict__ out) {
-  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
   const uint32_t lane = lane_id();
-  for (uint64_t u = warp; u < n; u += nwarps) {
+  WARP_LOOP(u, n) {
     const uint64_t b = off[u];
     const uint32_t U = cnt[u];
     uint32_t live = 0;
@@ -369,6 +408,8 @@ __global__ void __launch_bounds__(kBlock)
     if (lane == 0) out[u] = live;
   }
 }
+
+#undef WARP_LOOP
 
 // ------------------------------------------------------------- host glue
 
@@ -380,23 +421,18 @@ unsigned grid_for(uint64_t items, unsigned block, unsigned cap = 1u << 20) {
 }
 
 unsigned warp_grid(rnndg_ctx* c, uint64_t items) {
-  // one warp per item, persistent: enough blocks to fill every SM twice over
+  // one warp per item, persistent: at most 16 blocks per SM
   uint64_t need = (items + kWarpsPerBlock - 1) / kWarpsPerBlock;
   uint64_t cap = uint64_t(sm_count(c)) * 16;
   if (need < 1) need = 1;
   return unsigned(need < cap ? need : cap);
 }
 
-void* cub_temp(rnndg_ctx* c, size_t bytes) {
-  return c->cub_tmp.ensure(bytes);
-}
+void* cub_temp(rnndg_ctx* c, size_t bytes) { return c->cub_tmp.ensure(bytes); }
 
-// exclusive scan of n u32 (or u64) counts into n+1 u64 offsets
+// exclusive scan of n counts into n+1 u64 offsets (out[n] = total; the input
+// array must have n+1 readable slots, the last one's value is irrelevant)
 void scan_u32(rnndg_ctx* c, const uint32_t* in, uint64_t* out, uint64_t n) {
-  // out[n] must be the total: scan n+1 items with a zero appended through
-  // the transform iterator reading in[n] is out of bounds, so scan n items
-  // and add the last element with a tiny kernel-free trick: scan n+1 over a
-  // count array whose last slot is zero (callers size arrays n+1).
   cub::TransformInputIterator<uint64_t, ToU64, const uint32_t*> it(in, ToU64{});
   size_t bytes = 0;
   RNNDG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, it, out, int64_t(n + 1), c->stream));
@@ -415,34 +451,30 @@ void scan_u64(rnndg_ctx* c, const unsigned long long* in, uint64_t* out, uint64_
 }
 
 // segments [begin[u], end[u]) of keys_in sorted ascending into keys_out
-void seg_sort_keys(rnndg_ctx* c, const uint64_t* keys_in, uint64_t* keys_out,
-                   uint64_t span, uint64_t nseg, const uint64_t* begin,
-                   const uint64_t* end) {
+void seg_sort_keys(rnndg_ctx* c, const uint64_t* keys_in, uint64_t* keys_out, uint64_t span,
+                   uint64_t nseg, const uint64_t* begin, const uint64_t* end) {
   if (span == 0 || nseg == 0) return;
   if (span > uint64_t(INT32_MAX)) throw CudaError("segmented sort span exceeds 2^31");
   size_t bytes = 0;
-  RNNDG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, keys_in, keys_out,
-                                                int(span), int(nseg), begin, end,
-                                                c->stream));
+  RNNDG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, bytes, keys_in, keys_out, int(span),
+                                                int(nseg), begin, end, c->stream));
   void* tmp = cub_temp(c, bytes);
   RNNDG_CUDA(cub::DeviceSegmentedSort::SortKeys(tmp, bytes, keys_in, keys_out, int(span),
                                                 int(nseg), begin, end, c->stream));
   c->launches += 3;
 }
 
-void seg_sort_pairs(rnndg_ctx* c, const uint64_t* kin, uint64_t* kout,
-                    const uint32_t* vin, uint32_t* vout, uint64_t span,
-                    uint64_t nseg, const uint64_t* begin, const uint64_t* end) {
+void seg_sort_pairs(rnndg_ctx* c, const uint64_t* kin, uint64_t* kout, const uint32_t* vin,
+                    uint32_t* vout, uint64_t span, uint64_t nseg, const uint64_t* begin,
+                    const uint64_t* end) {
   if (span == 0 || nseg == 0) return;
   if (span > uint64_t(INT32_MAX)) throw CudaError("segmented sort span exceeds 2^31");
   size_t bytes = 0;
   RNNDG_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, kin, kout, vin, vout,
-                                                 int(span), int(nseg), begin, end,
-                                                 c->stream));
+                                                 int(span), int(nseg), begin, end, c->stream));
   void* tmp = cub_temp(c, bytes);
-  RNNDG_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp, bytes, kin, kout, vin, vout,
-                                                 int(span), int(nseg), begin, end,
-                                                 c->stream));
+  RNNDG_CUDA(cub::DeviceSegmentedSort::SortPairs(tmp, bytes, kin, kout, vin, vout, int(span),
+                                                 int(nseg), begin, end, c->stream));
   c->launches += 3;
 }
 
@@ -451,46 +483,6 @@ uint64_t read_u64(rnndg_ctx* c, const uint64_t* dev) {
   RNNDG_CUDA(cudaMemcpyAsync(&v, dev, sizeof(v), cudaMemcpyDeviceToHost, c->stream));
   RNNDG_CUDA(cudaStreamSynchronize(c->stream));
   return v;
-}
-
-// Build graph B from (post lists, buckets) and make it the current graph.
-// new_cnt must already be in c->cnt_b.
-void rebuild_and_swap(rnndg_ctx* c, const uint8_t* active, const uint32_t* post_cnt,
-                      const uint64_t* boff, const uint64_t* bkey,
-                      const uint8_t* bflag) {
-  const uint64_t n = c->n;
-  c->off_b.ensure(n + 1);
-  scan_u32(c, c->cnt_b.p, c->off_b.p, n);
-  const uint64_t total = read_u64(c, c->off_b.p + n);
-  c->key_b.ensure(total ? total : 1);
-  RNNDG_LAUNCH(c, k_rebuild, warp_grid(c, n), kBlock, 0, n, c->off.p, active, c->key.p,
-               c->key_s.p, post_cnt, boff, bkey, bflag, c->off_b.p, c->key_b.p);
-  c->off.swap(c->off_b);
-  c->key.swap(c->key_b);
-  c->cnt.swap(c->cnt_b);
-  c->span = total;
-}
-
-void ensure_scratch(rnndg_ctx* c) {
-  const uint64_t n = c->n, span = c->span ? c->span : 1;
-  c->active.ensure(n);
-  c->act_list.ensure(2 * n);
-  c->work.ensure(2);
-  c->post_cnt.ensure(n + 1);
-  c->cnt_b.ensure(n + 1);
-  c->seg_end.ensure(n);
-  c->bcnt.ensure(n + 1);
-  c->bcur.ensure(n);
-  c->boff.ensure(n + 1);
-  c->counters.ensure(kNumCounters);
-  c->key_s.ensure(span);
-  c->pend_src.ensure(span);
-  c->pend_key.ensure(span);
-  c->touch.ensure(span);
-  c->kpos_g.ensure(span);
-  c->kpos2_g.ensure(span);
-  c->bkey.ensure(span);
-  c->bflag.ensure(span);
 }
 
 template <class T>
@@ -502,6 +494,86 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
   float ms = 0.f;
   RNNDG_CUDA(cudaEventElapsedTime(&ms, a, b));
   return ms;
+}
+
+void ensure_scratch(rnndg_ctx* c) {
+  const uint64_t n = c->n, span = c->span ? c->span : 1;
+  c->active.ensure(n);
+  c->act_list.ensure(2 * n);
+  c->post_cnt.ensure(n + 1);
+  c->cnt_b.ensure(n + 1);
+  c->seg_end.ensure(n);
+  c->bcnt.ensure(n + 1);
+  c->bcur.ensure(n);
+  c->boff.ensure(n + 1);
+  c->counters.ensure(kNumCounters);
+  c->work.ensure(4);
+  c->label.ensure(2 * n);
+  c->okey.ensure(2 * n);
+  c->act_small.ensure(n);
+  c->key_s.ensure(span);
+  c->pend_src.ensure(span);
+  c->pend_key.ensure(span);
+  c->touch.ensure(span);
+  c->kpos_g.ensure(span);
+  c->kpos2_g.ensure(span);
+  c->bkey.ensure(span);
+  c->bkey_s.ensure(span);
+  c->bflag.ensure(span);
+  c->brank.ensure(span);
+}
+
+// Sort each bucket [boff[u], boff[u+1]) of bkey into bkey_s.
+void sort_buckets(rnndg_ctx* c, uint64_t total) {
+  if (total == 0) return;
+  seg_sort_keys(c, c->bkey.p, c->bkey_s.p, total, c->n, c->boff.p, c->boff.p + 1);
+}
+
+// Build graph B = merge(current lists with post_cnt, sorted buckets) and make
+// it the current graph.  New counts must be in c->cnt_b.
+void merge_and_swap(rnndg_ctx* c, const uint32_t* post_cnt) {
+  const uint64_t n = c->n;
+  c->off_b.ensure(n + 1);
+  scan_u32(c, c->cnt_b.p, c->off_b.p, n);
+  const uint64_t total = read_u64(c, c->off_b.p + n);
+  c->key_b.ensure(total ? total : 1);
+  RNNDG_LAUNCH(c, k_merge, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p, post_cnt,
+               c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->off_b.p, c->key_b.p);
+  c->off.swap(c->off_b);
+  c->key.swap(c->key_b);
+  c->cnt.swap(c->cnt_b);
+  c->span = total;
+}
+
+// Locality order of the short active lists into c->act_small; count into
+// work[2] (read by the scan kernel).
+void locality_order(rnndg_ctx* c) {
+  const uint64_t n = c->n;
+  uint32_t* la = c->label.p;
+  uint32_t* lb = c->label.p + n;
+  RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
+               nullptr, la);
+  for (int r = 1; r < kLabelRounds; ++r) {
+    RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
+                 la, lb);
+    std::swap(la, lb);
+  }
+  uint64_t* ok = c->okey.p;
+  uint64_t* ok2 = c->okey.p + n;
+  RNNDG_LAUNCH(c, k_order_keys, grid_for(n, 256), 256, 0, n, la, ok);
+  size_t bytes = 0;
+  RNNDG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, ok, ok2, int64_t(n), 0, 64,
+                                            c->stream));
+  RNNDG_CUDA(cub::DeviceRadixSort::SortKeys(cub_temp(c, bytes), bytes, ok, ok2, int64_t(n), 0,
+                                            64, c->stream));
+  c->launches += 8;
+  int* nsel = reinterpret_cast<int*>(c->work.p + 2);
+  bytes = 0;
+  RNNDG_CUDA(cub::DeviceSelect::If(nullptr, bytes, ok2, c->act_small.p, nsel, int64_t(n),
+                                   IsShortActive{c->active.p}, c->stream));
+  RNNDG_CUDA(cub::DeviceSelect::If(cub_temp(c, bytes), bytes, ok2, c->act_small.p, nsel,
+                                   int64_t(n), IsShortActive{c->active.p}, c->stream));
+  c->launches += 2;
 }
 
 }  // namespace
@@ -525,13 +597,14 @@ void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
   c->key.ensure(c->span);
   RNNDG_LAUNCH(c, k_fill_offsets, grid_for(n + 1, 256), 256, 0, n, S, c->off.p, c->cnt.p);
   if (c->d % 4 == 0)
-    RNNDG_LAUNCH(c, k_random_init<true>, warp_grid(c, n), kBlock, 0, n, S, seed, c->x,
-                 c->d, c->key.p);
+    RNNDG_LAUNCH(c, k_random_init<true>, warp_grid(c, n), kBlock, 0, n, S, seed, c->x, c->d,
+                 c->key.p);
   else
-    RNNDG_LAUNCH(c, k_random_init<false>, warp_grid(c, n), kBlock, 0, n, S, seed, c->x,
-                 c->d, c->key.p);
+    RNNDG_LAUNCH(c, k_random_init<false>, warp_grid(c, n), kBlock, 0, n, S, seed, c->x, c->d,
+                 c->key.p);
   c->has_graph = true;
   c->has_distances = true;
+  op_sort_lists(c);  // establish the sorted-list invariant
 }
 
 void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_sort,
@@ -540,26 +613,25 @@ void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_s
   ensure_scratch(c);
   unsigned long long* ctr = c->counters.p;
   zero(c, ctr, kNumCounters);
+  zero(c, c->work.p, 4);
   zero(c, c->pend_src.p, c->span, 0xFF);
   zero(c, c->touch.p, c->span);
   zero(c, c->bcnt.p, n + 1);
   zero(c, c->bcur.p, n);
   RNNDG_CUDA(cudaEventRecord(c->ev[0], c->stream));
-  RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p,
-               c->key.p, c->active.p, c->seg_end.p, c->act_list.p, c->post_cnt.p, ctr);
-  seg_sort_keys(c, c->key.p, c->key_s.p, c->span, n, c->off.p, c->seg_end.p);
+  RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
+               c->active.p, c->act_list.p, c->post_cnt.p, ctr);
+  locality_order(c);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
-  // distance stage: push-formulated scan, one warp per vertex (scan.cu)
-  zero(c, c->work.p, 2);
   launch_scan(c, c->work.p);
   RNNDG_CUDA(cudaEventRecord(c->ev[2], c->stream));
   scan_u64(c, c->bcnt.p, c->boff.p, n);
   RNNDG_LAUNCH(c, k_pend_scatter, grid_for(c->span, 256, 148 * 64), 256, 0, c->span,
                c->pend_src.p, c->pend_key.p, c->boff.p, c->bcur.p, c->bkey.p);
-  RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->active.p,
-               c->key.p, c->key_s.p, c->post_cnt.p, c->boff.p, c->bkey.p, c->bflag.p,
-               c->cnt_b.p, 1, ctr);
-  rebuild_and_swap(c, c->active.p, c->post_cnt.p, c->boff.p, c->bkey.p, c->bflag.p);
+  sort_buckets(c, c->span);
+  RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p,
+               c->post_cnt.p, c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, ctr, 1);
+  merge_and_swap(c, c->post_cnt.p);
   RNNDG_CUDA(cudaEventRecord(c->ev[3], c->stream));
   unsigned long long h[kNumCounters];
   RNNDG_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -574,35 +646,31 @@ void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_s
   if (t_scan) *t_scan += elapsed_ms(c->ev[1], c->ev[2]) * 1e-3;
   if (t_apply) *t_apply += elapsed_ms(c->ev[2], c->ev[3]) * 1e-3;
   if (touched) *touched += h[kTouched];
+  if (active_entries) *active_entries += h[kActiveEntries];
   if (c->trace)
     std::fprintf(stderr,
                  "[rnndg] pass active=%llu large=%llu maxlen=%llu entries=%llu checks=%llu "
-                 "removed=%llu inserted=%llu touched=%llu sort=%.3fms scan=%.3fms apply=%.3fms\n",
+                 "removed=%llu inserted=%llu touched=%llu order=%.3fms scan=%.3fms apply=%.3fms\n",
                  h[kActiveCount], h[kLargeCount], h[kMaxLen], h[kActiveEntries], h[kPairChecks],
                  h[kRemoved], h[kInserted], h[kTouched], elapsed_ms(c->ev[0], c->ev[1]),
                  elapsed_ms(c->ev[1], c->ev[2]), elapsed_ms(c->ev[2], c->ev[3]));
-  if (active_entries) *active_entries += h[kActiveEntries];
 }
 
 namespace {
 
 void out_prune(rnndg_ctx* c, uint32_t R) {
-  const uint64_t n = c->n;
-  RNNDG_LAUNCH(c, k_seg_end, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, nullptr, R,
-               c->seg_end.p);
-  seg_sort_keys(c, c->key.p, c->key_s.p, c->span, n, c->off.p, c->seg_end.p);
-  RNNDG_LAUNCH(c, k_out_take, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
-               c->key_s.p, c->key.p, R);
+  RNNDG_LAUNCH(c, k_out_trunc, grid_for(c->n, 256), 256, 0, c->n, c->cnt.p, R);
 }
 
 void in_prune(rnndg_ctx* c, uint32_t R) {
   const uint64_t n = c->n;
   zero(c, c->bcnt.p, n + 1);
   zero(c, c->bcur.p, n);
-  RNNDG_LAUNCH(c, k_count_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
-               c->key.p, c->bcnt.p);
+  RNNDG_LAUNCH(c, k_count_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
+               c->bcnt.p);
   scan_u64(c, c->bcnt.p, c->boff.p, n);
   const uint64_t m = read_u64(c, c->boff.p + n);
+  if (c->span >= (1ull << 32)) throw CudaError("in_prune: edge slots exceed 2^32");
   c->bkey.ensure(m ? m : 1);
   c->bkey_s.ensure(m ? m : 1);
   c->bpay.ensure(m ? m : 1);
@@ -613,11 +681,19 @@ void in_prune(rnndg_ctx* c, uint32_t R) {
                c->seg_end.p);
   seg_sort_pairs(c, c->bkey.p, c->bkey_s.p, c->bpay.p, c->bpay_s.p, m, n, c->boff.p,
                  c->seg_end.p);
-  RNNDG_LAUNCH(c, k_in_mark, warp_grid(c, n), kBlock, 0, n, c->boff.p, c->bpay_s.p,
-               c->key.p, R);
-  RNNDG_LAUNCH(c, k_count_live, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
-               c->key.p, c->cnt_b.p);
-  rebuild_and_swap(c, nullptr, c->cnt.p, nullptr, nullptr, nullptr);
+  RNNDG_LAUNCH(c, k_in_mark, warp_grid(c, n), kBlock, 0, n, c->boff.p, c->bpay_s.p, c->key.p, R);
+  RNNDG_LAUNCH(c, k_count_live, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
+               c->cnt_b.p);
+  c->off_b.ensure(n + 1);
+  scan_u32(c, c->cnt_b.p, c->off_b.p, n);
+  const uint64_t total = read_u64(c, c->off_b.p + n);
+  c->key_b.ensure(total ? total : 1);
+  RNNDG_LAUNCH(c, k_compact, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
+               c->off_b.p, c->key_b.p);
+  c->off.swap(c->off_b);
+  c->key.swap(c->key_b);
+  c->cnt.swap(c->cnt_b);
+  c->span = total;
 }
 
 }  // namespace
@@ -630,19 +706,21 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
   // 1. reversals bucketed by their source (= target of the forward edge)
   zero(c, c->bcnt.p, n + 1);
   zero(c, c->bcur.p, n);
-  RNNDG_LAUNCH(c, k_count_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
-               c->key.p, c->bcnt.p);
+  RNNDG_LAUNCH(c, k_count_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
+               c->bcnt.p);
   scan_u64(c, c->bcnt.p, c->boff.p, n);
   const uint64_t m = read_u64(c, c->boff.p + n);
   c->bkey.ensure(m ? m : 1);
+  c->bkey_s.ensure(m ? m : 1);
   c->bflag.ensure(m ? m : 1);
+  c->brank.ensure(m ? m : 1);
   RNNDG_LAUNCH(c, k_scatter_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p,
                c->key.p, c->boff.p, c->bcur.p, c->bkey.p, nullptr, 0);
+  sort_buckets(c, m);
   // 2. append-if-absent (no duplicates among reversals: edges are unique)
-  RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, nullptr,
-               c->key.p, nullptr, c->cnt.p, c->boff.p, c->bkey.p, c->bflag.p,
-               c->cnt_b.p, 0, c->counters.p);
-  rebuild_and_swap(c, nullptr, c->cnt.p, c->boff.p, c->bkey.p, c->bflag.p);
+  RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p, c->cnt.p,
+               c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, c->counters.p, 0);
+  merge_and_swap(c, c->cnt.p);
   ensure_scratch(c);  // span grew
   // 3. degree caps (builder.cpp:244-250)
   if (order == RNNDG_OUT_THEN_IN) {
@@ -650,7 +728,6 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
     in_prune(c, R);
   } else {
     in_prune(c, R);
-    ensure_scratch(c);
     out_prune(c, R);
   }
 }

@@ -104,6 +104,8 @@ struct rnndg_ctx {
 
   // pass scratch
   rnndg::DevBuf<uint8_t> active, touch, bflag;
+  rnndg::DevBuf<uint32_t> label, brank;
+  rnndg::DevBuf<uint64_t> okey, act_small;
   rnndg::DevBuf<uint32_t> act_list, pend_src, bpay, bpay_s;
   rnndg::DevBuf<uint64_t> pend_key, bkey, bkey_s, seg_end, boff;
   rnndg::DevBuf<unsigned long long> bcnt, bcur;

@@ -351,8 +351,8 @@ void op_search(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t L,
   if (k < 1 || k > L) throw ParamError("search: k out of [1, L]");
   if (entry_mode == RNNDG_ENTRY_FIXED && entry_vertex >= n)
     throw ParamError("search: entry vertex out of range");
-  // select_nearest needs lists nearest-first when distances are cached
-  if (c->has_distances) op_sort_lists(c);
+  // select_nearest: lists are kept nearest-first when distances are cached
+  // (sorted-list invariant, build.cu) and in stored order otherwise
 
   SearchArgs a{};
   a.x = c->x;
@@ -508,7 +508,6 @@ uint32_t op_rng_strategy(rnndg_ctx* c, uint32_t u, const uint32_t* cand_ids,
 }
 
 void op_degree_stats(rnndg_ctx* c, uint32_t cap, uint64_t out[3]) {
-  if (c->has_distances && cap) op_sort_lists(c);
   DevBuf<unsigned int> indeg;
   DevBuf<unsigned long long> o;
   indeg.ensure(c->n);

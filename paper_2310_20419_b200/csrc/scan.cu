@@ -191,7 +191,9 @@ __device__ __forceinline__ void emit_redirect(uint64_t base, uint32_t q, uint64_
 }
 
 struct ScanArgs {
-  const uint32_t* act_list;
+  const uint64_t* act_small;  // short active lists, locality order (low 32 bits = vertex)
+  const int* nsmall;
+  const uint32_t* act_list;   // act_list[n ..): long active lists
   uint64_t n;
   const unsigned long long* ctr_in;
   unsigned int* work;
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_push(ScanArgs g) {
   const uint32_t lane = lane_id();
   const uint32_t wib = threadIdx.x >> 5;
   const unsigned below = (1u << lane) - 1u;
-  const uint32_t nact = uint32_t(g.ctr_in[kActiveCount]);
+  const uint32_t nact = uint32_t(*g.nsmall);
   const Row row = g.row;  // local copy (no generic pointers into param space)
   const uint32_t row_bytes = row.stride * 4u;
   uint64_t* K = keys_sh[wib];
@@ -246,7 +248,7 @@ __global__ void __launch_bounds__(kThreads) k_scan_push(ScanArgs g) {
     if (lane == 0) a = atomicAdd(g.work, 1u);
     a = __shfl_sync(0xffffffffu, a, 0);
     if (a >= nact) break;
-    const uint32_t u = g.act_list[a];
+    const uint32_t u = uint32_t(g.act_small[a]);
     const uint64_t base = g.off[u];
     const uint32_t U = g.cnt[u];
     uint64_t* L = g.keys + base;
@@ -413,18 +415,21 @@ void prepare_chain_layout(rnndg_ctx* c) {
 }
 
 // Launches both scan kernels; the long-list kernel runs on the side stream
-// and is joined back before returning.  work[0] / work[1] are the queues.
+// and is joined back before returning.  work[0] / work[1] are the queues,
+// work[2] the number of short active lists.
 void launch_scan(rnndg_ctx* c, unsigned int* work) {
   const ScanConfig cfg = scan_config(c);
   prepare_chain_layout(c);
   ScanArgs a{};
+  a.act_small = c->act_small.p;
+  a.nsmall = reinterpret_cast<const int*>(work + 2);
   a.act_list = c->act_list.p;
   a.n = c->n;
   a.ctr_in = c->counters.p;
   a.work = work;
   a.off = c->off.p;
   a.cnt = c->cnt.p;
-  a.keys = c->key_s.p;
+  a.keys = c->key.p;  // lists are scanned in place (sorted invariant)
   a.row = Row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail};
   a.alive_g = c->kpos_g.p;
   a.alive2_g = c->kpos2_g.p;
