@@ -49,9 +49,10 @@ void check(int rc) {
   throw std::runtime_error(msg);
 }
 
+// The store is uploaded on every call: the caller may mutate or reallocate
+// it between calls (a cached pointer is not an identity).
 void bind_store(const VectorStore& s) {
   Ctx& c = ctx();
-  if (c.store == &s && c.data == s.data.data() && c.n == s.n && c.d == s.d) return;
   check(rnndg_set_data(c.h, s.data.data(), s.n, uint32_t(s.d)));
   c.store = &s;
   c.data = s.data.data();
@@ -97,7 +98,6 @@ void download(AdjacencyGraph& g) {
 // satisfies the context when the caller has not bound one
 void bind_any(size_t n) {
   Ctx& c = ctx();
-  if (c.store && c.n == n) return;
   static thread_local std::vector<float> zeros;
   zeros.assign(n ? n : 1, 0.0f);
   check(rnndg_set_data(c.h, zeros.data(), n ? n : 1, 1));

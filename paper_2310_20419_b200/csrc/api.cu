@@ -340,6 +340,7 @@ int rnndg_set_graph(rnndg_ctx* c, uint64_t n, const uint64_t* offsets, const uin
     c->span = m;
     c->has_graph = true;
     c->has_distances = dists != nullptr;
+    c->exact_dists = false;  // caller-provided distances: id-based membership
     // graphs with cached distances keep every list sorted by (dist, id)
     // (build.cu invariant); a graph loaded without distances keeps its stored
     // order, which select_nearest then uses (graph.cpp:65-74)

@@ -223,14 +223,16 @@ __global__ void k_pend_scatter(uint64_t span, const uint32_t* __restrict__ pend_
 // vertex, on a bucket sorted by key.  A proposal is dropped when it equals the
 // previous proposal (duplicate redirects carry bit-identical keys, so keeping
 // one equals the reference's sort + unique) or when the post list already
-// holds the same (dist, id).  brank = exclusive rank among kept proposals.
+// holds the same (dist, id) -- or, when the cached distances came from the
+// caller and are not known to be exact, the same id (has_target,
+// builder.cpp:22-26).  brank = exclusive rank among kept proposals.
 __global__ void __launch_bounds__(kBlock)
     k_apply_count(uint64_t n, const uint64_t* __restrict__ off,
                   const uint64_t* __restrict__ key, const uint32_t* __restrict__ post_cnt,
                   const uint64_t* __restrict__ boff, const uint64_t* __restrict__ bkey,
                   uint8_t* __restrict__ bflag, uint32_t* __restrict__ brank,
                   uint32_t* __restrict__ new_cnt, unsigned long long* __restrict__ ctr,
-                  int count_inserted) {
+                  int count_inserted, int exact) {
   const uint32_t lane = lane_id();
   unsigned long long inserted = 0;
   WARP_LOOP(u, n) {
@@ -250,8 +252,15 @@ __global__ void __launch_bounds__(kBlock)
         const bool dup = xi > b0 && bkey[xi - 1] == k;
         bool present = false;
         if (!dup) {
-          const uint32_t pos = lower_bound(P, pc, k & ~1ull);
-          present = pos < pc && (P[pos] >> 1) == (k >> 1);
+          if (exact) {
+            const uint32_t pos = lower_bound(P, pc, k & ~1ull);
+            present = pos < pc && (P[pos] >> 1) == (k >> 1);
+          } else {
+            // caller-provided distances: match on the id alone, exactly as
+            // has_target (builder.cpp:22-26)
+            const uint32_t id = key_id(k);
+            for (uint32_t j = 0; j < pc && !present; ++j) present = key_id(P[j]) == id;
+          }
         }
         keep = !dup && !present;
         bflag[xi] = keep ? 0 : 1;
@@ -516,7 +525,6 @@ void ensure_scratch(rnndg_ctx* c) {
   c->pend_key.ensure(span);
   c->touch.ensure(span);
   c->kpos_g.ensure(span);
-  c->kpos2_g.ensure(span);
   c->bkey.ensure(span);
   c->bkey_s.ensure(span);
   c->bflag.ensure(span);
@@ -604,6 +612,7 @@ void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
                  c->key.p);
   c->has_graph = true;
   c->has_distances = true;
+  c->exact_dists = true;
   op_sort_lists(c);  // establish the sorted-list invariant
 }
 
@@ -630,7 +639,8 @@ void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_s
                c->pend_src.p, c->pend_key.p, c->boff.p, c->bcur.p, c->bkey.p);
   sort_buckets(c, c->span);
   RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p,
-               c->post_cnt.p, c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, ctr, 1);
+               c->post_cnt.p, c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, ctr, 1,
+               int(c->exact_dists));
   merge_and_swap(c, c->post_cnt.p);
   RNNDG_CUDA(cudaEventRecord(c->ev[3], c->stream));
   unsigned long long h[kNumCounters];
@@ -719,7 +729,8 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
   sort_buckets(c, m);
   // 2. append-if-absent (no duplicates among reversals: edges are unique)
   RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p, c->cnt.p,
-               c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, c->counters.p, 0);
+               c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, c->counters.p, 0,
+               int(c->exact_dists));
   merge_and_swap(c, c->cnt.p);
   ensure_scratch(c);  // span grew
   // 3. degree caps (builder.cpp:244-250)

@@ -101,6 +101,9 @@ struct rnndg_ctx {
   uint64_t span = 0;
   bool has_graph = false;
   bool has_distances = true;
+  // every cached dist is the exact l2 of its endpoints (true for graphs built
+  // here; false after rnndg_set_graph with caller-provided distances)
+  bool exact_dists = true;
 
   // pass scratch
   rnndg::DevBuf<uint8_t> active, touch, bflag;
@@ -112,7 +115,7 @@ struct rnndg_ctx {
   rnndg::DevBuf<uint32_t> post_cnt;
   rnndg::DevBuf<unsigned long long> counters;
   rnndg::DevBuf<unsigned int> work;
-  rnndg::DevBuf<uint32_t> kpos_g, kpos2_g;  // scan scratch for lists > kScanUcap
+  rnndg::DevBuf<uint32_t> kpos_g;  // scan scratch for lists > kScanUcap
   // chain-blocked copy of the store for the distance stage (scan.cu)
   rnndg::DevBuf<float> xp;
   const float* xp_src = nullptr;

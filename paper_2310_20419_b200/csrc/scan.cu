@@ -10,21 +10,23 @@
 // flag_skips (old/old pairs passed over), removed and each redirect
 // (w, v, d(v,w)) come out identical, with no speculative distance work.
 //
-// Mapping.  A push step's tests run 8 per warp at a time: one quad of lanes
-// per pair, one lane per fp32 chain.  The store is kept on the device in a
-// chain-blocked layout (k_chain_layout) so lane k reads chain k's next 8
-// elements with one 256-bit load (LDG.E.ENL2.256) and a quad reads a full
-// 128-byte line.  The chains are combined exactly as ((s0+s1)+(s2+s3)) and
-// the d % 4 tail is added in order (metric.hpp:15-24): bit-identical to
-// rnnd::l2_sq.  A vertex's rows are pulled into L2 with one bulk prefetch per
-// row (cp.async.bulk.prefetch.L2, UBLKPF) when its scan starts.
+// Mapping.  One CTA per active vertex (persistent CTAs, dynamic queue).  A
+// push step's tests are compacted into a task list and evaluated 8 per warp
+// at a time: one quad of lanes per pair, one lane per fp32 chain.  The store
+// is kept on the device in a chain-blocked layout (k_chain_layout) so lane k
+// reads chain k's next 8 elements with one 256-bit load (LDG.E.ENL2.256) and
+// a quad reads a full 128-byte line.  The chains are combined exactly as
+// ((s0+s1)+(s2+s3)) and the d % 4 tail is added in order (metric.hpp:15-24):
+// bit-identical to rnnd::l2_sq.  A vertex's rows are pulled into L2 with one
+// bulk prefetch per row (cp.async.bulk.prefetch.L2, UBLKPF) when it starts.
 //
-//   k_scan_push      one warp per vertex, lists <= kScanUcap: sorted keys and
-//                    the alive list live in shared memory
-//   k_scan_push_cta  one 1024-thread CTA per vertex for longer lists (hubs that
-//                    collect redirects); every push step is split over 32
-//                    warps.  Runs concurrently with k_scan_push on a second
-//                    stream.
+// Spreading a step over a CTA (instead of one warp) shortens each vertex's
+// lifetime, so fewer vertices are in flight and their rows stay in L2 between
+// push steps (ncu: a warp-per-vertex scan re-read rows from HBM at every step).
+//
+//   k_scan_block<4, false>   lists <= kScanUcap; keys + alive list in smem
+//   k_scan_block<32, true>   longer lists (hubs that collect redirects), on a
+//                            second stream concurrently
 #include "common.cuh"
 #include "ctx.hpp"
 #include "scan.cuh"
@@ -33,10 +35,8 @@ namespace rnndg {
 
 namespace {
 
-constexpr int kWarps = 8;
-constexpr int kThreads = 32 * kWarps;
-constexpr int kBigThreads = 1024;
-constexpr int kBigWarps = kBigThreads / 32;
+constexpr int kShortWarps = 4;   // one 128-thread CTA per short list
+constexpr int kLongWarps = 32;   // one 1024-thread CTA per long list
 
 // Chain-blocked row layout: element e < d4 = d - d % 4 lives at
 //   32 * (e / 32) + 8 * (e % 4) + (e % 32) / 4
@@ -137,59 +137,6 @@ struct Row {
   }
 };
 
-// One push round: the lanes' candidates (valid, key vk at list position q)
-// against the kept entry wk.  Returns whether this lane's candidate is removed
-// (and the occluding distance).  Accumulates the reference counters in lane 0
-// and marks touched list positions.
-__device__ __forceinline__ bool push_round(const Row& row, bool valid, uint32_t q, uint64_t vk,
-                                           uint64_t wk, uint32_t p, const float* xw, uint8_t* T,
-                                           float& dvw, unsigned long long& checks,
-                                           unsigned long long& skips) {
-  const uint32_t lane = lane_id();
-  const uint32_t quad = lane >> 2, chain = lane & 3;
-  const bool need = valid && (key_fresh(wk) || key_fresh(vk));  // builder.cpp:53-56
-  const unsigned m_valid = __ballot_sync(0xffffffffu, valid);
-  const unsigned m_need = __ballot_sync(0xffffffffu, need);
-  const uint32_t n_need = __popc(m_need);
-  if (lane == 0) {
-    skips += __popc(m_valid & ~m_need);
-    checks += n_need;
-  }
-  const uint32_t my_rank = __popc(m_need & ((1u << lane) - 1u));
-  const uint32_t first = __ffs(m_need) - 1;
-  bool gone = false;
-  for (uint32_t r0 = 0; r0 < n_need; r0 += 8) {
-    // quad j evaluates the (r0 + j)-th needed candidate of the round; quads
-    // without a task repeat the first one (keeps the shuffles uniform)
-    const uint32_t src = __fns(m_need, 0, int(r0 + quad + 1));
-    const bool has = src < 32u;
-    const uint32_t s = has ? src : first;
-    const uint32_t qs = __shfl_sync(0xffffffffu, q, s);
-    const uint64_t vks = __shfl_sync(0xffffffffu, vk, s);
-    const float dist = quad_l2(row(vks), xw, chain, row.nblk, row.ntail);
-    if (has && chain == 0) {
-      T[qs] = 1;
-      T[p] = 1;
-    }
-    const bool mine = need && my_rank >= r0 && my_rank < r0 + 8;
-    const float dq = __shfl_sync(0xffffffffu, dist, mine ? 4 * (my_rank - r0) : 0);
-    if (mine) {
-      dvw = dq;
-      gone = key_dist(vk) >= dq;
-    }
-  }
-  return gone;
-}
-
-__device__ __forceinline__ void emit_redirect(uint64_t base, uint32_t q, uint64_t vk, uint64_t wk,
-                                              float dvw, uint32_t* pend_src, uint64_t* pend_key,
-                                              unsigned long long* bcnt) {
-  const uint32_t w_id = key_id(wk);
-  pend_src[base + q] = w_id;
-  pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
-  atomicAdd(&bcnt[w_id], 1ull);
-}
-
 struct ScanArgs {
   const uint64_t* act_small;  // short active lists, locality order (low 32 bits = vertex)
   const int* nsmall;
@@ -202,7 +149,6 @@ struct ScanArgs {
   uint64_t* keys;
   Row row;
   uint32_t* alive_g;
-  uint32_t* alive2_g;
   uint8_t* touch;
   uint32_t* post_cnt;
   uint32_t* pend_src;
@@ -229,162 +175,137 @@ __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned
   }
 }
 
-// ---------------------------------------------------------------- small
-__global__ void __launch_bounds__(kThreads) k_scan_push(ScanArgs g) {
-  __shared__ uint64_t keys_sh[kWarps][kScanUcap];
-  __shared__ uint32_t alive_sh[kWarps][kScanUcap];
-  const uint32_t lane = lane_id();
-  const uint32_t wib = threadIdx.x >> 5;
-  const unsigned below = (1u << lane) - 1u;
-  const uint32_t nact = uint32_t(*g.nsmall);
+// Order-preserving block-wide compaction index of `pred`; total in `total`.
+template <int W>
+__device__ __forceinline__ uint32_t block_rank(bool pred, uint32_t* wcnt, uint32_t& total) {
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  const unsigned m = __ballot_sync(0xffffffffu, pred);
+  if (lane == 0) wcnt[wid] = __popc(m);
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const uint32_t c = wcnt[w];
+    before += uint32_t(w) < wid ? c : 0u;
+    tot += c;
+  }
+  total = tot;
+  __syncthreads();
+  return before + __popc(m & ((1u << lane) - 1u));
+}
+
+// One CTA of W warps scans one vertex at a time (persistent, dynamic queue).
+// A push step walks the alive candidates in batches of 32*W: the needed pairs
+// of a batch are compacted into a task list and evaluated 8*W at a time (a
+// quad per pair, a lane per chain), so a step with up to 8*W needed pairs
+// costs one distance latency.  kLong: lists longer than kScanUcap, whose keys
+// and alive list stay in global memory (queue act_list[n ..), work[1]);
+// otherwise keys and alive list live in shared memory (queue act_small,
+// work[0]).
+template <int W, bool kLong>
+__global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
+  constexpr uint32_t NT = 32 * W;
+  constexpr uint32_t kCap = kLong ? 1 : kScanUcap;
+  __shared__ uint64_t keys_sh[kCap];
+  __shared__ uint32_t alive_sh[kCap];
+  __shared__ uint32_t tq[NT];   // task: list position of the candidate
+  __shared__ uint64_t tk[NT];   //       its key
+  __shared__ float tres[NT];    //       its distance to the kept entry
+  __shared__ uint32_t wcnt[W];
+  __shared__ uint32_t s_a;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  const uint32_t quad = lane >> 2, chain = lane & 3;
   const Row row = g.row;  // local copy (no generic pointers into param space)
   const uint32_t row_bytes = row.stride * 4u;
-  uint64_t* K = keys_sh[wib];
-  uint32_t* A = alive_sh[wib];
+  const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount]) : uint32_t(*g.nsmall);
   unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
 
   for (;;) {
-    uint32_t a = 0;
-    if (lane == 0) a = atomicAdd(g.work, 1u);
-    a = __shfl_sync(0xffffffffu, a, 0);
-    if (a >= nact) break;
-    const uint32_t u = uint32_t(g.act_small[a]);
+    if (tid == 0) s_a = atomicAdd(g.work + (kLong ? 1 : 0), 1u);
+    __syncthreads();
+    const uint32_t a = s_a;
+    if (a >= nq) break;
+    const uint32_t u = kLong ? g.act_list[g.n + a] : uint32_t(g.act_small[a]);
     const uint64_t base = g.off[u];
     const uint32_t U = g.cnt[u];
     uint64_t* L = g.keys + base;
     uint8_t* T = g.touch + base;
-    for (uint32_t j = lane; j < U; j += 32) {
+    // kLong: keys are read from L directly; the kept entry of a step is
+    // written to L[nk] with nk <= p < every alive position, so no alive key
+    // is overwritten
+    const uint64_t* K = kLong ? L : keys_sh;
+    uint32_t* A = kLong ? g.alive_g + base : alive_sh;
+    for (uint32_t j = tid; j < U; j += NT) {
       const uint64_t k = L[j];
-      K[j] = k;
+      if (!kLong) keys_sh[j] = k;
       A[j] = j;
       prefetch_row_l2(row(k), row_bytes);
     }
-    __syncwarp();
+    __syncthreads();
     uint32_t na = U, nk = 0;
     while (na) {
       // the first alive candidate is kept: every earlier kept entry has
       // already been tested against it
       const uint32_t p = A[0];
       const uint64_t wk = K[p];
+      const bool wf = key_fresh(wk);
       const float* xw = row(wk);
-      if (lane == 0) L[nk] = wk & ~1ull;  // flagged old (builder.cpp:68)
+      __syncthreads();  // all threads have read A[0] / K[p]
+      if (tid == 0) L[nk] = wk & ~1ull;  // flagged old (builder.cpp:68)
       ++nk;
-      uint32_t nn = 0;  // survivors, compacted into A[0 ..) in order
-      for (uint32_t g0 = 1; g0 < na; g0 += 32) {
-        const uint32_t gi = g0 + lane;
-        const bool valid = gi < na;
-        const uint32_t q = valid ? A[gi] : 0u;
+      uint32_t nn = 0;  // survivors so far, compacted in place into A[0 ..)
+      for (uint32_t b0 = 1; b0 < na; b0 += NT) {
+        const uint32_t ai = b0 + tid;
+        const bool valid = ai < na;
+        const uint32_t q = valid ? A[ai] : 0u;
         const uint64_t vk = valid ? K[q] : 0ull;
-        float dvw = 0.f;
-        const bool gone = push_round(row, valid, q, vk, wk, p, xw, T, dvw, checks, skips);
-        if (gone) {
-          ++removed;
-          emit_redirect(base, q, vk, wk, dvw, g.pend_src, g.pend_key, g.bcnt);
+        const bool need = valid && (wf || key_fresh(vk));  // builder.cpp:53-56
+        skips += (valid && !need) ? 1 : 0;
+        uint32_t ntask;
+        const uint32_t t = block_rank<W>(need, wcnt, ntask);
+        if (need) {
+          tq[t] = q;
+          tk[t] = vk;
         }
-        const bool stay = valid && !gone;
-        const unsigned m_stay = __ballot_sync(0xffffffffu, stay);
-        __syncwarp();
-        if (stay) A[nn + __popc(m_stay & below)] = q;
-        nn += __popc(m_stay);
-        __syncwarp();
+        checks += need ? 1 : 0;
+        __syncthreads();
+        for (uint32_t t0 = 0; t0 < ntask; t0 += 8 * W) {
+          const uint32_t tw = t0 + 8 * wid;
+          if (tw >= ntask) continue;  // warp-uniform
+          const uint32_t ti = tw + quad;
+          const bool has = ti < ntask;
+          const uint64_t ks = tk[has ? ti : tw];
+          const float dist = quad_l2(row(ks), xw, chain, row.nblk, row.ntail);
+          if (has && chain == 0) {
+            tres[ti] = dist;
+            T[tq[ti]] = 1;
+            T[p] = 1;
+          }
+        }
+        __syncthreads();
+        bool gone = false;
+        if (need) {
+          const float dvw = tres[t];
+          gone = key_dist(vk) >= dvw;
+          if (gone) {
+            ++removed;
+            const uint32_t w_id = key_id(wk);
+            g.pend_src[base + q] = w_id;
+            g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
+            atomicAdd(&g.bcnt[w_id], 1ull);
+          }
+        }
+        uint32_t nstay;
+        const uint32_t r = block_rank<W>(valid && !gone, wcnt, nstay);
+        // every thread of the batch has read its A[ai] (block_rank syncs)
+        if (valid && !gone) A[nn + r] = q;
+        nn += nstay;
+        __syncthreads();
       }
       na = nn;
     }
-    if (lane == 0) g.post_cnt[u] = nk;
-    for (uint32_t j = lane; j < U; j += 32) touched += T[j];
-    __syncwarp();
-  }
-  flush_counters(g.ctr, removed, checks, skips, touched);
-}
-
-// ------------------------------------------------------------------ big
-// One CTA per long list.  Each push step: thread 0's view of A[0] is the kept
-// entry; the alive candidates A[1 .. na) are split into contiguous ranges,
-// one per warp; survivors are compacted per warp into A2 and then gathered,
-// in order, back into A.
-__global__ void __launch_bounds__(kBigThreads) k_scan_push_cta(ScanArgs g) {
-  __shared__ uint32_t wcount[kBigWarps];
-  __shared__ uint32_t wstart[kBigWarps];
-  __shared__ uint32_t s_a, s_na;
-  const uint32_t lane = lane_id();
-  const uint32_t wid = threadIdx.x >> 5;
-  const unsigned below = (1u << lane) - 1u;
-  const uint32_t nlarge = uint32_t(g.ctr_in[kLargeCount]);
-  const Row row = g.row;
-  const uint32_t row_bytes = row.stride * 4u;
-  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
-
-  for (;;) {
-    if (threadIdx.x == 0) s_a = atomicAdd(g.work + 1, 1u);
-    __syncthreads();
-    const uint32_t a = s_a;
-    if (a >= nlarge) break;
-    const uint32_t u = g.act_list[g.n + a];
-    const uint64_t base = g.off[u];
-    const uint32_t U = g.cnt[u];
-    uint64_t* L = g.keys + base;
-    uint8_t* T = g.touch + base;
-    uint32_t* A = g.alive_g + base;
-    uint32_t* A2 = g.alive2_g + base;
-    for (uint32_t j = threadIdx.x; j < U; j += kBigThreads) {
-      A[j] = j;
-      prefetch_row_l2(row(L[j]), row_bytes);
-    }
-    if (threadIdx.x == 0) s_na = U;
-    __syncthreads();
-    uint32_t nk = 0;
-    // The kept entry of a step is written to L[nk] in place; L[q] for alive
-    // q > p is never overwritten (nk <= p), so candidates read keys from L.
-    for (;;) {
-      const uint32_t na = s_na;
-      if (na == 0) break;
-      const uint32_t p = A[0];
-      const uint64_t wk = L[p];
-      const float* xw = row(wk);
-      __syncthreads();  // everyone has read A[0] and L[p]
-      if (threadIdx.x == 0) L[nk] = wk & ~1ull;
-      ++nk;
-      // warp w takes candidates [1 + w*span, 1 + (w+1)*span)
-      const uint32_t ncand = na - 1;
-      const uint32_t span = ((ncand + kBigWarps - 1) / kBigWarps + 31) & ~31u;
-      const uint32_t lo = 1 + wid * span;
-      const uint32_t hi = lo + span < na ? lo + span : na;
-      uint32_t nn = 0;
-      for (uint32_t g0 = lo; g0 < hi; g0 += 32) {
-        const uint32_t gi = g0 + lane;
-        const bool valid = gi < hi;
-        const uint32_t q = valid ? A[gi] : 0u;
-        const uint64_t vk = valid ? L[q] : 0ull;
-        float dvw = 0.f;
-        const bool gone = push_round(row, valid, q, vk, wk, p, xw, T, dvw, checks, skips);
-        if (gone) {
-          ++removed;
-          emit_redirect(base, q, vk, wk, dvw, g.pend_src, g.pend_key, g.bcnt);
-        }
-        const bool stay = valid && !gone;
-        const unsigned m_stay = __ballot_sync(0xffffffffu, stay);
-        if (stay) A2[lo - 1 + nn + __popc(m_stay & below)] = q;
-        nn += __popc(m_stay);
-      }
-      if (lane == 0) wcount[wid] = lo < na ? nn : 0u;
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        uint32_t t = 0;
-        for (int w = 0; w < kBigWarps; ++w) {
-          wstart[w] = t;
-          t += wcount[w];
-        }
-        s_na = t;
-      }
-      __syncthreads();
-      if (lo < na) {
-        const uint32_t cnt_w = wcount[wid], dst = wstart[wid];
-        for (uint32_t j = lane; j < cnt_w; j += 32) A[dst + j] = A2[lo - 1 + j];
-      }
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) g.post_cnt[u] = nk;
-    for (uint32_t j = threadIdx.x; j < U; j += kBigThreads) touched += T[j];
+    if (tid == 0) g.post_cnt[u] = nk;
+    for (uint32_t j = tid; j < U; j += NT) touched += T[j];
     __syncthreads();
   }
   flush_counters(g.ctr, removed, checks, skips, touched);
@@ -432,7 +353,6 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   a.keys = c->key.p;  // lists are scanned in place (sorted invariant)
   a.row = Row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail};
   a.alive_g = c->kpos_g.p;
-  a.alive2_g = c->kpos2_g.p;
   a.touch = c->touch.p;
   a.post_cnt = c->post_cnt.p;
   a.pend_src = c->pend_src.p;
@@ -441,15 +361,16 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   a.ctr = c->counters.p;
   static thread_local int per_sm = 0;
   if (!per_sm)
-    RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_push, kThreads, 0));
+    RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, k_scan_block<kShortWarps, false>, 32 * kShortWarps, 0));
   const unsigned grid = unsigned(sm_count(c)) * unsigned(per_sm > 0 ? per_sm : 1);
-  // fork: side stream waits for everything issued so far on the main stream
+  // fork: the side stream waits for everything issued so far on the main one
   RNNDG_CUDA(cudaEventRecord(c->ev_fork, c->stream));
   RNNDG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-  k_scan_push_cta<<<unsigned(sm_count(c)) / 4, kBigThreads, 0, c->side>>>(a);
+  k_scan_block<kLongWarps, true><<<unsigned(sm_count(c)) / 4, 32 * kLongWarps, 0, c->side>>>(a);
   ++c->launches;
   RNNDG_CUDA(cudaGetLastError());
-  RNNDG_LAUNCH(c, k_scan_push, grid, kThreads, 0, a);
+  RNNDG_LAUNCH(c, (k_scan_block<kShortWarps, false>), grid, 32 * kShortWarps, 0, a);
   RNNDG_CUDA(cudaEventRecord(c->ev_join, c->side));
   RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
 }
