@@ -130,6 +130,7 @@ struct rnndg_ctx {
 
   std::vector<rnndg_counts> pass_counts;
   bool trace = false;  // RNNDG_TRACE=1: per-pass line on stderr
+  bool scan_cfg_logged = false;
   // timing events
   cudaEvent_t ev[8] = {};
 };

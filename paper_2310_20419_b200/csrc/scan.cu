@@ -27,6 +27,9 @@
 //   k_scan_block<4, false>   lists <= kScanUcap; keys + alive list in smem
 //   k_scan_block<32, true>   longer lists (hubs that collect redirects), on a
 //                            second stream concurrently
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "ctx.hpp"
 #include "scan.cuh"
@@ -129,6 +132,77 @@ __device__ __forceinline__ float quad_l2(const float* __restrict__ a, const floa
   return sum;
 }
 
+// Same as quad_l2 on generic pointers (rows staged in shared memory or in
+// global memory): two 128-bit loads per block and operand.
+__device__ __forceinline__ float quad_l2_any(const float* a, const float* b, uint32_t k,
+                                             uint32_t nblk, uint32_t ntail) {
+  float s = 0.f;
+  const float4* pa = reinterpret_cast<const float4*>(a + 8 * k);
+  const float4* pb = reinterpret_cast<const float4*>(b + 8 * k);
+#pragma unroll 4
+  for (uint32_t blk = 0; blk < nblk; ++blk) {
+    const float4 a0 = pa[8 * blk], a1 = pa[8 * blk + 1];
+    const float4 b0 = pb[8 * blk], b1 = pb[8 * blk + 1];
+    const float va[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+    const float vb[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+    chain_step(va, vb, s);
+  }
+  const float s_next = __shfl_down_sync(0xffffffffu, s, 1);
+  const float pair = __fadd_rn(s, s_next);
+  const float pair2 = __shfl_down_sync(0xffffffffu, pair, 2);
+  float sum = __fadd_rn(pair, pair2);
+  if (ntail && k == 0) {
+    const float* ta = a + 32 * nblk;
+    const float* tb = b + 32 * nblk;
+    for (uint32_t t = 0; t < ntail; ++t) {
+      const float df = __fsub_rn(ta[t], tb[t]);
+      sum = __fadd_rn(sum, __fmul_rn(df, df));
+    }
+  }
+  return sum;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
+// 1-D TMA bulk copy global -> shared, completion counted on `bar` in bytes
+__device__ __forceinline__ void tma_load(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
 struct Row {
   const float* xp;
   uint32_t stride, nblk, ntail;
@@ -149,6 +223,8 @@ struct ScanArgs {
   uint64_t* keys;
   Row row;
   uint32_t* alive_g;
+  uint32_t nslots;       // row slots in dynamic shared memory (kStage)
+  uint32_t slot_floats;  // slot stride
   uint8_t* touch;
   uint32_t* post_cnt;
   uint32_t* pend_src;
@@ -202,8 +278,10 @@ __device__ __forceinline__ uint32_t block_rank(bool pred, uint32_t* wcnt, uint32
 // and alive list stay in global memory (queue act_list[n ..), work[1]);
 // otherwise keys and alive list live in shared memory (queue act_small,
 // work[0]).
-template <int W, bool kLong>
+template <int W, bool kLong, bool kStage>
 __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  float* slots = reinterpret_cast<float*>(dyn_smem);
   constexpr uint32_t NT = 32 * W;
   constexpr uint32_t kCap = kLong ? 1 : kScanUcap;
   __shared__ uint64_t keys_sh[kCap];
@@ -213,12 +291,18 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
   __shared__ float tres[NT];    //       its distance to the kept entry
   __shared__ uint32_t wcnt[W];
   __shared__ uint32_t s_a;
+  __shared__ uint64_t bar;
   const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
   const uint32_t quad = lane >> 2, chain = lane & 3;
   const Row row = g.row;  // local copy (no generic pointers into param space)
   const uint32_t row_bytes = row.stride * 4u;
   const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount]) : uint32_t(*g.nsmall);
   unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
+  uint32_t parity = 0;
+  if (kStage && tid == 0) {
+    mbar_init(&bar, 1);
+    fence_proxy_async();
+  }
 
   for (;;) {
     if (tid == 0) s_a = atomicAdd(g.work + (kLong ? 1 : 0), 1u);
@@ -235,13 +319,32 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
     // is overwritten
     const uint64_t* K = kLong ? L : keys_sh;
     uint32_t* A = kLong ? g.alive_g + base : alive_sh;
+    // kStage: the nearest min(U, nslots) rows go to shared-memory slots with
+    // one TMA bulk copy each (HBM read once per scanned vertex); the rest are
+    // read through L2, prefetched in bulk
+    const uint32_t nst = kStage ? (U < g.nslots ? U : g.nslots) : 0u;
     for (uint32_t j = tid; j < U; j += NT) {
       const uint64_t k = L[j];
       if (!kLong) keys_sh[j] = k;
       A[j] = j;
-      prefetch_row_l2(row(k), row_bytes);
+      if (j >= nst) prefetch_row_l2(row(k), row_bytes);
     }
     __syncthreads();
+    if (kStage) {
+      if (tid == 0 && nst) {
+        fence_proxy_async();  // earlier generic reads of the slots are done
+        mbar_arrive_expect_tx(&bar, nst * row_bytes);
+        for (uint32_t j = 0; j < nst; ++j)
+          tma_load(slots + size_t(j) * g.slot_floats, row(K[j]), row_bytes, &bar);
+      }
+      if (nst) {
+        mbar_wait(&bar, parity);
+        parity ^= 1u;
+      }
+    }
+    auto rowp = [&](uint32_t pos, uint64_t key) -> const float* {
+      return pos < nst ? slots + size_t(pos) * g.slot_floats : row(key);
+    };
     uint32_t na = U, nk = 0;
     while (na) {
       // the first alive candidate is kept: every earlier kept entry has
@@ -249,7 +352,7 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
       const uint32_t p = A[0];
       const uint64_t wk = K[p];
       const bool wf = key_fresh(wk);
-      const float* xw = row(wk);
+      const float* xw = rowp(p, wk);
       __syncthreads();  // all threads have read A[0] / K[p]
       if (tid == 0) L[nk] = wk & ~1ull;  // flagged old (builder.cpp:68)
       ++nk;
@@ -274,8 +377,10 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
           if (tw >= ntask) continue;  // warp-uniform
           const uint32_t ti = tw + quad;
           const bool has = ti < ntask;
-          const uint64_t ks = tk[has ? ti : tw];
-          const float dist = quad_l2(row(ks), xw, chain, row.nblk, row.ntail);
+          const uint32_t ts = has ? ti : tw;
+          const float* xv = rowp(tq[ts], tk[ts]);
+          const float dist = kStage ? quad_l2_any(xv, xw, chain, row.nblk, row.ntail)
+                                    : quad_l2(xv, xw, chain, row.nblk, row.ntail);
           if (has && chain == 0) {
             tres[ti] = dist;
             T[tq[ti]] = 1;
@@ -359,18 +464,45 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   a.pend_key = c->pend_key.p;
   a.bcnt = c->bcnt.p;
   a.ctr = c->counters.p;
-  static thread_local int per_sm = 0;
-  if (!per_sm)
-    RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, k_scan_block<kShortWarps, false>, 32 * kShortWarps, 0));
+  // row slots: stride padded to an odd multiple of 16 B (quads of two CTAs'
+  // rows land in different bank groups); ~100 KB per CTA for long rows
+  // (2 CTAs per SM), ~48 KB for short rows
+  a.slot_floats = cfg.stride + 4;
+  const size_t slot_bytes = size_t(a.slot_floats) * 4;
+  const size_t budget = slot_bytes >= 2048 ? 96 * 1024 : 48 * 1024;
+  size_t ns = budget / slot_bytes;
+  if (ns > kScanUcap) ns = kScanUcap;
+  a.nslots = uint32_t(ns);
+  // shared-memory staging of the nearest rows is an experiment (RNNDG_STAGE=1):
+  // at 2 CTAs per SM it measured slower than reading rows through L2
+  static const bool stage = [] {
+    const char* e = std::getenv("RNNDG_STAGE");
+    return e && e[0] == '1';
+  }();
+  if (!stage) a.nslots = 0;
+  const size_t smem = stage ? ns * slot_bytes : 0;
+  auto kshort = stage ? k_scan_block<kShortWarps, false, true>
+                      : k_scan_block<kShortWarps, false, false>;
+  if (smem > 48 * 1024) {
+    RNNDG_CUDA(cudaFuncSetAttribute(kshort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    RNNDG_CUDA(cudaFuncSetAttribute(kshort, cudaFuncAttributePreferredSharedMemoryCarveout,
+                                    cudaSharedmemCarveoutMaxShared));
+  }
+  int per_sm = 0;
+  RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kshort, 32 * kShortWarps, smem));
+  if (c->trace && !c->scan_cfg_logged) {
+    std::fprintf(stderr, "[rnndg] scan: stage=%d slots=%u smem=%zu B ctas/SM=%d\n", int(stage),
+                 a.nslots, smem, per_sm);
+    c->scan_cfg_logged = true;
+  }
   const unsigned grid = unsigned(sm_count(c)) * unsigned(per_sm > 0 ? per_sm : 1);
   // fork: the side stream waits for everything issued so far on the main one
   RNNDG_CUDA(cudaEventRecord(c->ev_fork, c->stream));
   RNNDG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-  k_scan_block<kLongWarps, true><<<unsigned(sm_count(c)) / 4, 32 * kLongWarps, 0, c->side>>>(a);
+  k_scan_block<kLongWarps, true, false><<<unsigned(sm_count(c)) / 4, 32 * kLongWarps, 0, c->side>>>(a);
   ++c->launches;
   RNNDG_CUDA(cudaGetLastError());
-  RNNDG_LAUNCH(c, (k_scan_block<kShortWarps, false>), grid, 32 * kShortWarps, 0, a);
+  RNNDG_LAUNCH(c, kshort, grid, 32 * kShortWarps, smem, a);
   RNNDG_CUDA(cudaEventRecord(c->ev_join, c->side));
   RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
 }
