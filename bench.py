@@ -31,7 +31,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
-CPU_SAMPLE_ROWS = 50_000
+CPU_SAMPLE_ROWS = 150_000
 METRIC = "RNN-Descent build L2 dist-evals/s (1M x 960 fp32, S=20 R=96 T1=4 T2=15)"
 
 

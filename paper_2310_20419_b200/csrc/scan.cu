@@ -68,7 +68,7 @@ __global__ void k_chain_layout(const float* __restrict__ x, uint64_t n, uint32_t
 }
 
 __device__ __forceinline__ void ld256(const float* p, float (&r)[8]) {
-  asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+  asm volatile("ld.global.nc.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
                  "=f"(r[6]), "=f"(r[7])
                : "l"(p));
