@@ -416,6 +416,195 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
   flush_counters(g.ctr, removed, checks, skips, touched);
 }
 
+// ------------------------------------------------------------- sliced
+// Short lists, rows staged per push round.  Each warp owns 8 pairs of a round
+// (one per quad) and streams their candidate rows through shared memory in
+// slices of kSliceBlk 32-float blocks with 1-D TMA bulk copies, double
+// buffered on two per-warp mbarriers; the kept row is staged once per step
+// per CTA.  A round therefore waits for ~2 memory latencies instead of one
+// per block, which shortens each vertex's lifetime and keeps its rows in L2
+// between push steps.
+constexpr uint32_t kSliceBlk = 4;
+constexpr uint32_t kSliceRow = kSliceBlk * 32 + 4;  // floats; +16 B spreads banks
+
+template <int W>
+__global__ void __launch_bounds__(32 * W) k_scan_sliced(ScanArgs g) {
+  constexpr uint32_t NT = 32 * W;
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  __shared__ uint64_t keys_sh[kScanUcap];
+  __shared__ uint32_t alive_sh[kScanUcap];
+  __shared__ uint32_t tq[NT];
+  __shared__ uint64_t tk[NT];
+  __shared__ float tres[NT];
+  __shared__ uint32_t wcnt[W];
+  __shared__ uint32_t s_a;
+  __shared__ __align__(8) uint64_t wbar;
+  __shared__ __align__(8) uint64_t vbar[W][2];
+  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  const uint32_t quad = lane >> 2, chain = lane & 3;
+  const Row row = g.row;
+  const uint32_t row_bytes = row.stride * 4u;
+  const uint32_t nblk = row.nblk;
+  const uint32_t nsl = (nblk + kSliceBlk - 1) / kSliceBlk;
+  float* wbuf = reinterpret_cast<float*>(dyn_smem);                       // row.stride floats
+  float* vbuf = wbuf + ((row.stride + 31) & ~31u) + size_t(wid) * 2 * 8 * kSliceRow;
+  const uint32_t nq = uint32_t(*g.nsmall);
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
+  uint32_t wpar = 0, vpar0 = 0, vpar1 = 0;
+  if (tid == 0) mbar_init(&wbar, 1);
+  if (lane == 0) {
+    mbar_init(&vbar[wid][0], 1);
+    mbar_init(&vbar[wid][1], 1);
+  }
+  fence_proxy_async();
+  __syncthreads();
+
+  // lane 0 of the warp: stage slice sl of the 8 (or fewer) task rows into buf
+  auto issue_slice = [&](uint32_t sl, uint32_t b, uint32_t tw, uint32_t nt_w) {
+    const uint32_t b0 = sl * kSliceBlk;
+    const uint32_t nb = nblk - b0 < kSliceBlk ? nblk - b0 : kSliceBlk;
+    const uint32_t bytes = nb * 128u;
+    fence_proxy_async();
+    mbar_arrive_expect_tx(&vbar[wid][b], bytes * nt_w);
+    for (uint32_t q = 0; q < nt_w; ++q)
+      tma_load(vbuf + size_t(b * 8 + q) * kSliceRow, row(tk[tw + q]) + 32 * b0, bytes,
+               &vbar[wid][b]);
+  };
+
+  for (;;) {
+    if (tid == 0) s_a = atomicAdd(g.work, 1u);
+    __syncthreads();
+    const uint32_t a = s_a;
+    if (a >= nq) break;
+    const uint32_t u = uint32_t(g.act_small[a]);
+    const uint64_t base = g.off[u];
+    const uint32_t U = g.cnt[u];
+    uint64_t* L = g.keys + base;
+    uint8_t* T = g.touch + base;
+    for (uint32_t j = tid; j < U; j += NT) {
+      const uint64_t k = L[j];
+      keys_sh[j] = k;
+      alive_sh[j] = j;
+      prefetch_row_l2(row(k), row_bytes);
+    }
+    __syncthreads();
+    uint32_t na = U, nk = 0;
+    while (na) {
+      const uint32_t p = alive_sh[0];
+      const uint64_t wk = keys_sh[p];
+      const bool wf = key_fresh(wk);
+      __syncthreads();  // all threads read alive_sh[0]; previous wbuf readers done
+      if (tid == 0) {
+        L[nk] = wk & ~1ull;  // flagged old (builder.cpp:68)
+        if (na > 1) {
+          fence_proxy_async();
+          mbar_arrive_expect_tx(&wbar, row_bytes);
+          tma_load(wbuf, row(wk), row_bytes, &wbar);
+        }
+      }
+      ++nk;
+      if (na > 1) {
+        mbar_wait(&wbar, wpar);
+        wpar ^= 1u;
+      }
+      uint32_t nn = 0;
+      for (uint32_t b0 = 1; b0 < na; b0 += NT) {
+        const uint32_t ai = b0 + tid;
+        const bool valid = ai < na;
+        const uint32_t q = valid ? alive_sh[ai] : 0u;
+        const uint64_t vk = valid ? keys_sh[q] : 0ull;
+        const bool need = valid && (wf || key_fresh(vk));  // builder.cpp:53-56
+        skips += (valid && !need) ? 1 : 0;
+        uint32_t ntask;
+        const uint32_t t = block_rank<W>(need, wcnt, ntask);
+        if (need) {
+          tq[t] = q;
+          tk[t] = vk;
+        }
+        checks += need ? 1 : 0;
+        __syncthreads();
+        for (uint32_t t0 = 0; t0 < ntask; t0 += 8 * W) {
+          const uint32_t tw = t0 + 8 * wid;
+          if (tw >= ntask) continue;  // warp-uniform
+          const uint32_t nt_w = ntask - tw < 8 ? ntask - tw : 8;
+          if (lane == 0) {
+            issue_slice(0, 0, tw, nt_w);
+            if (nsl > 1) issue_slice(1, 1, tw, nt_w);
+          }
+          float sacc = 0.f;
+          for (uint32_t sl = 0; sl < nsl; ++sl) {
+            const uint32_t b = sl & 1;
+            if (b == 0) {
+              mbar_wait(&vbar[wid][0], vpar0);
+              vpar0 ^= 1u;
+            } else {
+              mbar_wait(&vbar[wid][1], vpar1);
+              vpar1 ^= 1u;
+            }
+            const uint32_t bb = sl * kSliceBlk;
+            const uint32_t nb = nblk - bb < kSliceBlk ? nblk - bb : kSliceBlk;
+            const float* vs = vbuf + size_t(b * 8 + quad) * kSliceRow + 8 * chain;
+            const float* ws = wbuf + 32 * bb + 8 * chain;
+            for (uint32_t i = 0; i < nb; ++i) {
+              const float4 v0 = *reinterpret_cast<const float4*>(vs + 32 * i);
+              const float4 v1 = *reinterpret_cast<const float4*>(vs + 32 * i + 4);
+              const float4 w0 = *reinterpret_cast<const float4*>(ws + 32 * i);
+              const float4 w1 = *reinterpret_cast<const float4*>(ws + 32 * i + 4);
+              const float va[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+              const float vb[8] = {w0.x, w0.y, w0.z, w0.w, w1.x, w1.y, w1.z, w1.w};
+              chain_step(va, vb, sacc);
+            }
+            __syncwarp();
+            if (lane == 0 && sl + 2 < nsl) issue_slice(sl + 2, b, tw, nt_w);
+          }
+          const float s_next = __shfl_down_sync(0xffffffffu, sacc, 1);
+          const float pair = __fadd_rn(sacc, s_next);
+          const float pair2 = __shfl_down_sync(0xffffffffu, pair, 2);
+          float dist = __fadd_rn(pair, pair2);
+          const uint32_t ti = tw + quad;
+          const bool has = quad < nt_w;
+          if (has && chain == 0) {
+            if (row.ntail) {
+              const float* ta = row(tk[ti]) + 32 * nblk;
+              const float* tb = wbuf + 32 * nblk;
+              for (uint32_t x = 0; x < row.ntail; ++x) {
+                const float df = __fsub_rn(__ldg(ta + x), tb[x]);
+                dist = __fadd_rn(dist, __fmul_rn(df, df));
+              }
+            }
+            tres[ti] = dist;
+            T[tq[ti]] = 1;
+            T[p] = 1;
+          }
+        }
+        __syncthreads();
+        bool gone = false;
+        if (need) {
+          const float dvw = tres[t];
+          gone = key_dist(vk) >= dvw;
+          if (gone) {
+            ++removed;
+            const uint32_t w_id = key_id(wk);
+            g.pend_src[base + q] = w_id;
+            g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
+            atomicAdd(&g.bcnt[w_id], 1ull);
+          }
+        }
+        uint32_t nstay;
+        const uint32_t r = block_rank<W>(valid && !gone, wcnt, nstay);
+        if (valid && !gone) alive_sh[nn + r] = q;
+        nn += nstay;
+        __syncthreads();
+      }
+      na = nn;
+    }
+    if (tid == 0) g.post_cnt[u] = nk;
+    for (uint32_t j = tid; j < U; j += NT) touched += T[j];
+    __syncthreads();
+  }
+  flush_counters(g.ctr, removed, checks, skips, touched);
+}
+
 }  // namespace
 
 ScanConfig scan_config(rnndg_ctx* c) {
@@ -480,9 +669,21 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return e && e[0] == '1';
   }();
   if (!stage) a.nslots = 0;
-  const size_t smem = stage ? ns * slot_bytes : 0;
+  size_t smem = stage ? ns * slot_bytes : 0;
+  // experiment (RNNDG_SLICED=1): rows streamed through per-warp shared-memory
+  // slices with TMA; measured slower than direct 256-bit loads through L2
+  static const bool sliced = [] {
+    const char* e = std::getenv("RNNDG_SLICED");
+    return e && e[0] == '1';
+  }();
   auto kshort = stage ? k_scan_block<kShortWarps, false, true>
-                      : k_scan_block<kShortWarps, false, false>;
+                      : (sliced ? k_scan_sliced<kShortWarps>
+                                : k_scan_block<kShortWarps, false, false>);
+  size_t smem_sl = 0;
+  if (!stage && sliced) {
+    smem_sl = (size_t((cfg.stride + 31) & ~31u) + size_t(kShortWarps) * 2 * 8 * kSliceRow) * 4;
+    smem = smem_sl;
+  }
   if (smem > 48 * 1024) {
     RNNDG_CUDA(cudaFuncSetAttribute(kshort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     RNNDG_CUDA(cudaFuncSetAttribute(kshort, cudaFuncAttributePreferredSharedMemoryCarveout,
@@ -491,8 +692,8 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   int per_sm = 0;
   RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kshort, 32 * kShortWarps, smem));
   if (c->trace && !c->scan_cfg_logged) {
-    std::fprintf(stderr, "[rnndg] scan: stage=%d slots=%u smem=%zu B ctas/SM=%d\n", int(stage),
-                 a.nslots, smem, per_sm);
+    std::fprintf(stderr, "[rnndg] scan: stage=%d sliced=%d slots=%u smem=%zu B ctas/SM=%d\n",
+                 int(stage), int(sliced), a.nslots, smem, per_sm);
     c->scan_cfg_logged = true;
   }
   const unsigned grid = unsigned(sm_count(c)) * unsigned(per_sm > 0 ? per_sm : 1);
