@@ -605,6 +605,300 @@ __global__ void __launch_bounds__(32 * W) k_scan_sliced(ScanArgs g) {
   flush_counters(g.ctr, removed, checks, skips, touched);
 }
 
+// ------------------------------------------------------------------ pull
+// The reference's own ("pull") walk with a shared-memory row pool: a kept row
+// is tested by every later candidate, so kept rows stay in smem slots for the
+// whole scan of the vertex; candidate rows are TMA-loaded once.  HBM traffic
+// is therefore about one read per touched row (the algorithmic 4·d·T_p).
+// Candidates are processed in chunks of kCB; a wave evaluates, for every
+// pending candidate, its next kKSeg needed kept entries (and, in the first
+// wave of a chunk, every pair inside the chunk).  Warp 0 replays the
+// reference walk: lane b walks candidate b's kept segment up to its first
+// occluder (exact counters and redirect), lane 0 then resolves the
+// intra-chunk part in order.  Pairs past an occluder are speculation.
+constexpr uint32_t kCB = 8;
+constexpr uint32_t kKSeg = 16;
+constexpr uint32_t kPullTasks = kCB * kKSeg + kCB * (kCB - 1) / 2;
+constexpr uint32_t kPullMaxSlots = 256;
+constexpr uint16_t kNoSlot = 0xFFFF;
+enum : uint8_t { kStPending = 0, kStKept = 1, kStRemoved = 2 };
+
+template <int W>
+__global__ void __launch_bounds__(32 * W) k_scan_pull(ScanArgs g) {
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
+  float* slots = reinterpret_cast<float*>(dyn_smem);
+  __shared__ uint64_t keys_sh[kScanUcap];
+  __shared__ uint16_t rslot[kScanUcap];
+  __shared__ uint16_t kpos[kScanUcap];
+  __shared__ uint16_t fslot[kPullMaxSlots];
+  __shared__ uint16_t ta[kPullTasks], tb[kPullTasks], tinfo[kPullTasks];
+  __shared__ float tres[kPullTasks];
+  __shared__ float dint[kCB][kCB];
+  __shared__ uint16_t lpos[2 * kPullTasks];
+  __shared__ uint32_t cpos[kCB], cfront[kCB], cgen[kCB], cintra[kCB], tstart[kCB];
+  __shared__ uint8_t cstate[kCB];
+  __shared__ uint32_t s_a, s_nk, s_nfree, s_nt, s_loads, s_done;
+  __shared__ __align__(8) uint64_t bar;
+  constexpr uint32_t NT = 32 * W;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  const uint32_t quad = lane >> 2, chain = lane & 3;
+  const Row row = g.row;
+  const uint32_t row_bytes = row.stride * 4u;
+  const uint32_t nslots = g.nslots, sfl = g.slot_floats;
+  const uint32_t nq = uint32_t(*g.nsmall);
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
+  uint32_t parity = 0;
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    fence_proxy_async();
+  }
+  __syncthreads();
+
+  for (;;) {
+    if (tid == 0) s_a = atomicAdd(g.work, 1u);
+    __syncthreads();
+    const uint32_t a = s_a;
+    if (a >= nq) break;
+    const uint32_t u = uint32_t(g.act_small[a]);
+    const uint64_t base = g.off[u];
+    const uint32_t U = g.cnt[u];
+    uint64_t* L = g.keys + base;
+    uint8_t* T = g.touch + base;
+    for (uint32_t j = tid; j < U; j += NT) {
+      const uint64_t k = L[j];
+      keys_sh[j] = k;
+      rslot[j] = kNoSlot;
+      if (j >= nslots) prefetch_row_l2(row(k), row_bytes);
+    }
+    for (uint32_t j = tid; j < nslots; j += NT) fslot[j] = uint16_t(nslots - 1 - j);
+    if (tid == 0) {
+      s_nfree = nslots;
+      s_nk = 0;
+    }
+    __syncthreads();
+    auto rowp = [&](uint32_t pos) -> const float* {
+      const uint16_t sl = rslot[pos];
+      return sl != kNoSlot ? slots + size_t(sl) * sfl : row(keys_sh[pos]);
+    };
+
+    for (uint32_t pos = 0; pos < U; pos += kCB) {
+      const uint32_t nb = U - pos < kCB ? U - pos : kCB;
+      if (tid < nb) {
+        cpos[tid] = pos + tid;
+        cstate[tid] = kStPending;
+        cfront[tid] = 0;
+        cintra[tid] = 0;
+      }
+      __syncthreads();
+      const uint32_t k_old = s_nk;
+      bool first = true;
+      for (;;) {
+        // ---- task generation (warp 0: lane b owns candidate b)
+        if (wid == 0) {
+          const uint32_t b = lane;
+          const bool mine = b < nb && cstate[b] == kStPending;
+          const uint32_t vp = b < nb ? cpos[b] : 0u;
+          const bool vf = b < nb && key_fresh(keys_sh[vp]);
+          uint32_t nin = 0, nkt = 0, kend = 0;
+          if (b < nb && first)
+            for (uint32_t b2 = 0; b2 < b; ++b2) nin += (vf || key_fresh(keys_sh[cpos[b2]])) ? 1 : 0;
+          if (mine) {
+            uint32_t k = cfront[b];
+            while (k < k_old && nkt < kKSeg) {
+              nkt += (vf || key_fresh(keys_sh[kpos[k]])) ? 1 : 0;
+              ++k;
+            }
+            kend = k;
+          }
+          // exclusive prefix of (nin + nkt) over the lanes
+          uint32_t mycnt = nin + nkt, incl = mycnt;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= uint32_t(o)) incl += v;
+          }
+          const uint32_t off0 = incl - mycnt;
+          uint32_t t = off0;
+          if (b < nb && first)
+            for (uint32_t b2 = 0; b2 < b; ++b2)
+              if (vf || key_fresh(keys_sh[cpos[b2]])) {
+                ta[t] = uint16_t(vp);
+                tb[t] = uint16_t(cpos[b2]);
+                tinfo[t] = uint16_t(1 + b * kCB + b2);
+                ++t;
+              }
+          if (b < nb) tstart[b] = t;
+          if (mine) {
+            for (uint32_t k = cfront[b]; k < kend; ++k) {
+              const uint32_t wp = kpos[k];
+              if (vf || key_fresh(keys_sh[wp])) {
+                ta[t] = uint16_t(vp);
+                tb[t] = uint16_t(wp);
+                tinfo[t] = 0;
+                ++t;
+              }
+            }
+            cgen[b] = kend;
+          }
+          const uint32_t nt = __shfl_sync(0xffffffffu, incl, 31);
+          // rows this wave touches that are not resident: one thread assigns
+          // free slots and stages them with TMA
+          if (lane == 0) {
+            uint32_t loads = 0;
+            for (uint32_t x = 0; x < 2 * nt; ++x) {
+              const uint32_t pp = (x & 1) ? tb[x >> 1] : ta[x >> 1];
+              if (rslot[pp] != kNoSlot || s_nfree == 0) continue;
+              rslot[pp] = fslot[--s_nfree];
+              lpos[loads++] = uint16_t(pp);
+            }
+            if (loads) {
+              fence_proxy_async();
+              mbar_arrive_expect_tx(&bar, loads * row_bytes);
+              for (uint32_t i = 0; i < loads; ++i) {
+                const uint32_t pp = lpos[i];
+                tma_load(slots + size_t(rslot[pp]) * sfl, row(keys_sh[pp]), row_bytes, &bar);
+              }
+            }
+            s_loads = loads;
+            s_nt = nt;
+          }
+        }
+        __syncthreads();
+        const uint32_t nt = s_nt;
+        if (s_loads) {
+          mbar_wait(&bar, parity);
+          parity ^= 1u;
+        }
+        // ---- evaluate: a quad per pair, 8 pairs per warp per round
+        for (uint32_t t0 = 0; t0 < nt; t0 += 8 * W) {
+          const uint32_t tw = t0 + 8 * wid;
+          if (tw >= nt) continue;  // warp-uniform
+          const uint32_t ti = tw + quad;
+          const bool has = ti < nt;
+          const uint32_t ts = has ? ti : tw;
+          const float dist = quad_l2_any(rowp(ta[ts]), rowp(tb[ts]), chain, row.nblk, row.ntail);
+          if (has && chain == 0) {
+            tres[ti] = dist;
+            const uint32_t info = tinfo[ti];
+            if (info) dint[(info - 1) / kCB][(info - 1) % kCB] = dist;
+          }
+        }
+        __syncthreads();
+        // ---- replay the reference walk (warp 0)
+        if (wid == 0) {
+          const uint32_t b = lane;
+          if (b < nb && cstate[b] == kStPending) {
+            const uint32_t vp = cpos[b];
+            const uint64_t vk = keys_sh[vp];
+            const bool vf = key_fresh(vk);
+            const float vd = key_dist(vk);
+            uint32_t t = tstart[b];
+            bool gone = false;
+            for (uint32_t k = cfront[b]; k < cgen[b]; ++k) {
+              const uint32_t wp = kpos[k];
+              const uint64_t wk = keys_sh[wp];
+              if (!vf && !key_fresh(wk)) {
+                ++skips;
+                continue;
+              }
+              const float dvw = tres[t++];
+              ++checks;
+              T[vp] = 1;
+              T[wp] = 1;
+              if (vd >= dvw) {
+                gone = true;
+                cstate[b] = kStRemoved;
+                ++removed;
+                const uint32_t w_id = key_id(wk);
+                g.pend_src[base + vp] = w_id;
+                g.pend_key[base + vp] = make_key(dvw, key_id(vk), 1u);
+                atomicAdd(&g.bcnt[w_id], 1ull);
+                break;
+              }
+            }
+            if (!gone) cfront[b] = cgen[b];
+          }
+          __syncwarp();
+          if (lane == 0) {
+            // intra-chunk part, in candidate order: earlier chunk candidates
+            // that were kept come after K_old in the kept list
+            bool all_final = true;
+            for (uint32_t b2 = 0; b2 < nb; ++b2) {
+              if (cstate[b2] != kStPending) continue;
+              if (cfront[b2] < k_old) {
+                all_final = false;
+                continue;
+              }
+              const uint32_t vp = cpos[b2];
+              const uint64_t vk = keys_sh[vp];
+              const bool vf = key_fresh(vk);
+              const float vd = key_dist(vk);
+              bool gone = false, blocked = false;
+              for (uint32_t b3 = cintra[b2]; b3 < b2; ++b3) {
+                const uint8_t s3 = cstate[b3];
+                if (s3 == kStPending) {
+                  blocked = true;
+                  break;
+                }
+                cintra[b2] = b3 + 1;
+                if (s3 == kStRemoved) continue;
+                const uint32_t wp = cpos[b3];
+                const uint64_t wk = keys_sh[wp];
+                if (!vf && !key_fresh(wk)) {
+                  ++skips;
+                  continue;
+                }
+                const float dvw = dint[b2][b3];
+                ++checks;
+                T[vp] = 1;
+                T[wp] = 1;
+                if (vd >= dvw) {
+                  gone = true;
+                  cstate[b2] = kStRemoved;
+                  ++removed;
+                  const uint32_t w_id = key_id(wk);
+                  g.pend_src[base + vp] = w_id;
+                  g.pend_key[base + vp] = make_key(dvw, key_id(vk), 1u);
+                  atomicAdd(&g.bcnt[w_id], 1ull);
+                  break;
+                }
+              }
+              if (gone) continue;
+              if (blocked) {
+                all_final = false;
+                continue;
+              }
+              cstate[b2] = kStKept;
+            }
+            s_done = all_final ? 1u : 0u;
+            if (all_final) {
+              for (uint32_t b2 = 0; b2 < nb; ++b2) {
+                const uint32_t pp = cpos[b2];
+                if (cstate[b2] == kStKept) {
+                  kpos[s_nk++] = uint16_t(pp);
+                } else if (rslot[pp] != kNoSlot) {
+                  fslot[s_nfree++] = rslot[pp];
+                  rslot[pp] = kNoSlot;
+                }
+              }
+            }
+          }
+        }
+        first = false;
+        __syncthreads();
+        if (s_done) break;
+      }
+    }
+    // survivors, flagged old, become the post-scan list (builder.cpp:68)
+    const uint32_t nk = s_nk;
+    for (uint32_t k = tid; k < nk; k += NT) L[k] = keys_sh[kpos[k]] & ~1ull;
+    if (tid == 0) g.post_cnt[u] = nk;
+    for (uint32_t j = tid; j < U; j += NT) touched += T[j];
+    __syncthreads();
+  }
+  flush_counters(g.ctr, removed, checks, skips, touched);
+}
+
 }  // namespace
 
 ScanConfig scan_config(rnndg_ctx* c) {
@@ -676,21 +970,49 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     const char* e = std::getenv("RNNDG_SLICED");
     return e && e[0] == '1';
   }();
+  // default: push walk, rows through L2 (k_scan_block).  RNNDG_SCAN=pull
+  // selects the pull walk with a shared-memory row pool (k_scan_pull), which
+  // measured ~2x slower at d = 960 (too few CTAs per SM to hide its chunk
+  // loads); kept as an experiment
+  static const bool push = [] {
+    const char* e = std::getenv("RNNDG_SCAN");
+    return !(e && e[0] == 'p' && e[1] == 'u' && e[2] == 'l');
+  }();
+  // pull tuning knobs (experiments): RNNDG_PULL_W = warps per CTA (4|8),
+  // RNNDG_PULL_KB = shared-memory row pool per CTA in KB
+  static const int pull_w = [] {
+    const char* e = std::getenv("RNNDG_PULL_W");
+    return e && e[0] == '4' ? 4 : 8;
+  }();
+  static const int pull_kb = [] {
+    const char* e = std::getenv("RNNDG_PULL_KB");
+    return e ? std::atoi(e) : 0;
+  }();
   auto kshort = stage ? k_scan_block<kShortWarps, false, true>
                       : (sliced ? k_scan_sliced<kShortWarps>
-                                : k_scan_block<kShortWarps, false, false>);
+                                : (push ? k_scan_block<kShortWarps, false, false>
+                                        : (pull_w == 4 ? k_scan_pull<4> : k_scan_pull<8>)));
+  unsigned threads_short = 32 * (push || stage || sliced ? kShortWarps : pull_w);
+  if (!push && !stage && !sliced) {
+    const size_t pbudget = pull_kb > 0 ? size_t(pull_kb) * 1024
+                                       : (slot_bytes >= 2048 ? 150 * 1024 : 96 * 1024);
+    size_t pns = pbudget / slot_bytes;
+    if (pns > kPullMaxSlots) pns = kPullMaxSlots;
+    a.nslots = uint32_t(pns);
+    smem = pns * slot_bytes;
+  }
   size_t smem_sl = 0;
   if (!stage && sliced) {
     smem_sl = (size_t((cfg.stride + 31) & ~31u) + size_t(kShortWarps) * 2 * 8 * kSliceRow) * 4;
     smem = smem_sl;
   }
-  if (smem > 48 * 1024) {
+  if (smem > 0) {
     RNNDG_CUDA(cudaFuncSetAttribute(kshort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     RNNDG_CUDA(cudaFuncSetAttribute(kshort, cudaFuncAttributePreferredSharedMemoryCarveout,
                                     cudaSharedmemCarveoutMaxShared));
   }
   int per_sm = 0;
-  RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kshort, 32 * kShortWarps, smem));
+  RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kshort, threads_short, smem));
   if (c->trace && !c->scan_cfg_logged) {
     std::fprintf(stderr, "[rnndg] scan: stage=%d sliced=%d slots=%u smem=%zu B ctas/SM=%d\n",
                  int(stage), int(sliced), a.nslots, smem, per_sm);
@@ -703,7 +1025,7 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   k_scan_block<kLongWarps, true, false><<<unsigned(sm_count(c)) / 4, 32 * kLongWarps, 0, c->side>>>(a);
   ++c->launches;
   RNNDG_CUDA(cudaGetLastError());
-  RNNDG_LAUNCH(c, kshort, grid, 32 * kShortWarps, smem, a);
+  RNNDG_LAUNCH(c, kshort, grid, threads_short, smem, a);
   RNNDG_CUDA(cudaEventRecord(c->ev_join, c->side));
   RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
 }
