@@ -155,6 +155,40 @@ int rnndg_rng_strategy(rnndg_ctx* ctx, uint32_t u, const uint32_t* cand_ids,
 int rnndg_l2_pairs(rnndg_ctx* ctx, const uint32_t* a, const uint32_t* b,
                    uint64_t npairs, float* out);
 
+/* ---- sharded build ----
+ * Vertex ownership by contiguous ranges; the store is replicated on every
+ * rank.  One context owns vertices [v_begin, v_end).  A host-side driver
+ * (paper_2310_20419_b200/sharded.py) runs the protocol and moves records
+ * between owners with an all-to-all (NCCL, gloo or in-process):
+ *   pass:     shard_scan -> export -> all-to-all -> import(PENDING)
+ *   reverse:  stage(PROPOSAL) -> export -> all-to-all -> import(PROPOSAL);
+ *             out_prune; stage(INEDGE) -> ... -> import(INEDGE, R) stages the
+ *             deletions -> export -> ... -> import(DELETE)
+ * A record is (dst: global vertex id, key: list entry for dst's list).
+ * Every step is set-canonical, so the sharded graph equals the unsharded one
+ * entry for entry. */
+#define RNNDG_X_PENDING 0  /* redirect (w, v, d(v,w)) -> owner(w) */
+#define RNNDG_X_PROPOSAL 1 /* reverse proposal (v, u, d) -> owner(v) */
+#define RNNDG_X_INEDGE 2   /* in-edge (t, s, d) -> owner(t) */
+#define RNNDG_X_DELETE 3   /* in_prune deletion (s, t, d) -> owner(s) */
+
+int rnndg_set_partition(rnndg_ctx* ctx, uint64_t v_begin, uint64_t v_end);
+/* mark + scan of the owned lists; `partial` gets removed / flag_skips /
+ * pair_checks of this shard; the redirects are staged as records */
+int rnndg_shard_scan(rnndg_ctx* ctx, rnndg_counts* partial, uint64_t* nrecords);
+/* stage reverse proposals or in-edges of the owned lists */
+int rnndg_shard_stage(rnndg_ctx* ctx, int kind, uint64_t* nrecords);
+/* staged records sorted by dst into DEVICE buffers (nrecords each) and the
+ * number of records per destination part (bounds: parts+1 vertex ids) */
+int rnndg_shard_export(rnndg_ctx* ctx, const uint64_t* bounds, uint32_t parts,
+                       uint32_t* dst_dev, uint64_t* key_dev, uint64_t* counts);
+/* apply received records (DEVICE buffers); INEDGE stages deletions and
+ * returns their number in *nstaged; PENDING reports `inserted` */
+int rnndg_shard_import(rnndg_ctx* ctx, int kind, const uint32_t* dst_dev,
+                       const uint64_t* key_dev, uint64_t nrecords, uint32_t R,
+                       rnndg_counts* partial, uint64_t* nstaged);
+int rnndg_shard_out_prune(rnndg_ctx* ctx, uint32_t R);
+
 /* ---- synthetic inputs (host, no GPU needed) ---- */
 uint32_t rnndg_synth_dim(int cfg);
 int rnndg_synth(int cfg, uint64_t seed, uint64_t row0, uint64_t nrows,

@@ -12,6 +12,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "librnndg.so")
 
 OK, EPARAM, EDATA, EINTERNAL = 0, 1, 2, 3
+X_PENDING, X_PROPOSAL, X_INEDGE, X_DELETE = 0, 1, 2, 3
 
 u8p = C.POINTER(C.c_uint8)
 u32p = C.POINTER(C.c_uint32)
@@ -79,6 +80,13 @@ def lib() -> C.CDLL:
         "rnndg_rng_strategy": (C.c_int, [vp, C.c_uint32, u32p, f32p, C.c_uint32, u32p,
                                          f32p, u32p]),
         "rnndg_l2_pairs": (C.c_int, [vp, u32p, u32p, C.c_uint64, f32p]),
+        "rnndg_set_partition": (C.c_int, [vp, C.c_uint64, C.c_uint64]),
+        "rnndg_shard_scan": (C.c_int, [vp, C.POINTER(Counts), u64p]),
+        "rnndg_shard_stage": (C.c_int, [vp, C.c_int, u64p]),
+        "rnndg_shard_export": (C.c_int, [vp, u64p, C.c_uint32, vp, vp, u64p]),
+        "rnndg_shard_import": (C.c_int, [vp, C.c_int, vp, vp, C.c_uint64, C.c_uint32,
+                                         C.POINTER(Counts), u64p]),
+        "rnndg_shard_out_prune": (C.c_int, [vp, C.c_uint32]),
         "rnndg_synth_dim": (C.c_uint32, [C.c_int]),
         "rnndg_synth": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, f32p]),
     }
@@ -102,4 +110,6 @@ EXPORTED = (
     "rnndg_pass_counts", "rnndg_graph_size", "rnndg_get_graph", "rnndg_set_graph",
     "rnndg_index_bytes", "rnndg_degree_stats", "rnndg_search", "rnndg_brute_force",
     "rnndg_rng_strategy", "rnndg_l2_pairs", "rnndg_synth_dim", "rnndg_synth",
+    "rnndg_set_partition", "rnndg_shard_scan", "rnndg_shard_stage", "rnndg_shard_export",
+    "rnndg_shard_import", "rnndg_shard_out_prune",
 )

@@ -62,7 +62,7 @@ uint32_t crc32_ieee(const uint8_t* p, size_t size) {
 // device CSR (capacity layout) -> host (counts, keys) in list order
 void fetch_graph(rnndg_ctx* c, std::vector<uint64_t>& off, std::vector<uint32_t>& cnt,
                  std::vector<uint64_t>& keys) {
-  const uint64_t n = c->n;
+  const uint64_t n = c->nv;
   off.resize(n + 1);
   cnt.resize(n);
   RNNDG_CUDA(cudaMemcpyAsync(off.data(), c->off.p, (n + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
@@ -140,6 +140,9 @@ int rnndg_set_data(rnndg_ctx* c, const float* rows, uint64_t n, uint32_t d) {
     c->x = c->x_own.p;
     c->n = n;
     c->d = d;
+    c->v0 = 0;
+    c->nv = n;
+    c->partitioned = false;
     c->has_graph = false;
     c->xp_src = nullptr;  // chain-blocked copy is stale
   });
@@ -155,6 +158,9 @@ int rnndg_set_data_device(rnndg_ctx* c, const float* rows_dev, uint64_t n, uint3
     c->x = rows_dev;
     c->n = n;
     c->d = d;
+    c->v0 = 0;
+    c->nv = n;
+    c->partitioned = false;
     c->has_graph = false;
     c->xp_src = nullptr;
   });
@@ -268,12 +274,13 @@ int rnndg_pass_counts(const rnndg_ctx* c, rnndg_counts* out, uint32_t cap) {
 int rnndg_graph_size(rnndg_ctx* c, uint64_t* n, uint64_t* edges) {
   return guarded(c, [&] {
     need_graph(c);
-    std::vector<uint32_t> cnt(c->n);
-    RNNDG_CUDA(cudaMemcpyAsync(cnt.data(), c->cnt.p, c->n * 4, cudaMemcpyDeviceToHost, c->stream));
+    std::vector<uint32_t> cnt(c->nv);
+    if (c->nv)
+      RNNDG_CUDA(cudaMemcpyAsync(cnt.data(), c->cnt.p, c->nv * 4, cudaMemcpyDeviceToHost, c->stream));
     RNNDG_CUDA(cudaStreamSynchronize(c->stream));
     uint64_t m = 0;
     for (uint32_t v : cnt) m += v;
-    if (n) *n = c->n;
+    if (n) *n = c->nv;
     if (edges) *edges = m;
   });
 }
@@ -286,7 +293,7 @@ int rnndg_get_graph(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists
     std::vector<uint32_t> cnt;
     fetch_graph(c, off, cnt, keys);
     uint64_t w = 0;
-    for (uint64_t u = 0; u < c->n; ++u) {
+    for (uint64_t u = 0; u < c->nv; ++u) {
       if (offsets) offsets[u] = w;
       for (uint32_t j = 0; j < cnt[u]; ++j, ++w) {
         const uint64_t k = keys[off[u] + j];
@@ -295,7 +302,7 @@ int rnndg_get_graph(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists
         if (fresh) fresh[w] = uint8_t(key_fresh(k));
       }
     }
-    if (offsets) offsets[c->n] = w;
+    if (offsets) offsets[c->nv] = w;
   });
 }
 
@@ -303,7 +310,7 @@ int rnndg_set_graph(rnndg_ctx* c, uint64_t n, const uint64_t* offsets, const uin
                     const float* dists, const uint8_t* fresh) {
   return guarded(c, [&] {
     need_data(c);
-    if (n != c->n) throw DataError("set_graph: graph size does not match the store");
+    if (n != c->nv) throw DataError("set_graph: graph size does not match the store");
     if (!offsets) throw ParamError("set_graph: offsets required");
     if (offsets[0] != 0) throw DataError("set_graph: bad offsets");
     for (uint64_t u = 0; u < n; ++u)
@@ -319,8 +326,8 @@ int rnndg_set_graph(rnndg_ctx* c, uint64_t n, const uint64_t* offsets, const uin
       cnt[u] = uint32_t(b - a);
       scratch.assign(ids + a, ids + b);
       for (uint64_t j = a; j < b; ++j) {
-        if (ids[j] >= n) throw DataError("set_graph: id out of range");
-        if (ids[j] == u) throw DataError("set_graph: self-loop");
+        if (ids[j] >= c->n) throw DataError("set_graph: id out of range");
+        if (ids[j] == c->v0 + u) throw DataError("set_graph: self-loop");
         float dv = dists ? dists[j] : 0.0f;
         if (dists && !(dv >= 0.0f)) throw DataError("set_graph: distance must be >= 0");
         if (dv == 0.0f) dv = 0.0f;  // canonical +0
@@ -357,7 +364,7 @@ int rnndg_index_bytes(rnndg_ctx* c, uint8_t* buf, uint64_t* size) {
     fetch_graph(c, off, cnt, keys);
     uint64_t m = 0;
     for (uint32_t v : cnt) m += v;
-    const uint64_t total = 16 + (c->n + 1) * 8 + m * 4 + 4;
+    const uint64_t total = 16 + (c->nv + 1) * 8 + m * 4 + 4;
     if (size) *size = total;
     if (!buf) return;
     // graph.cpp:102-126: "RNND", u32 version 1, u64 n, u64 offsets[n+1],
@@ -373,14 +380,14 @@ int rnndg_index_bytes(rnndg_ctx* c, uint8_t* buf, uint64_t* size) {
     std::memcpy(p, "RNND", 4);
     p += 4;
     put32(1);
-    put64(c->n);
+    put64(c->nv);
     uint64_t o = 0;
     put64(o);
-    for (uint64_t u = 0; u < c->n; ++u) {
+    for (uint64_t u = 0; u < c->nv; ++u) {
       o += cnt[u];
       put64(o);
     }
-    for (uint64_t u = 0; u < c->n; ++u)
+    for (uint64_t u = 0; u < c->nv; ++u)
       for (uint32_t j = 0; j < cnt[u]; ++j) put32(key_id(keys[off[u] + j]));
     put32(crc32_ieee(buf, size_t(p - buf)));
   });
@@ -429,6 +436,65 @@ int rnndg_l2_pairs(rnndg_ctx* c, const uint32_t* a, const uint32_t* b, uint64_t 
     for (uint64_t i = 0; i < npairs; ++i)
       if (a[i] >= c->n || b[i] >= c->n) throw ParamError("l2_pairs: id out of range");
     op_l2_pairs(c, a, b, npairs, out);
+  });
+}
+
+int rnndg_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end) {
+  return guarded(c, [&] {
+    need_data(c);
+    op_set_partition(c, v_begin, v_end);
+  });
+}
+
+int rnndg_shard_scan(rnndg_ctx* c, rnndg_counts* partial, uint64_t* nrecords) {
+  return guarded(c, [&] {
+    need_graph(c);
+    if (!c->has_distances) throw ParamError("update_neighbors: graph has no distances");
+    rnndg_counts cc{};
+    const uint64_t m = op_shard_scan(c, &cc, nullptr, nullptr);
+    if (partial) *partial = cc;
+    if (nrecords) *nrecords = m;
+  });
+}
+
+int rnndg_shard_stage(rnndg_ctx* c, int kind, uint64_t* nrecords) {
+  return guarded(c, [&] {
+    need_graph(c);
+    if (kind != RNNDG_X_PROPOSAL && kind != RNNDG_X_INEDGE)
+      throw ParamError("shard_stage: kind must be PROPOSAL or INEDGE");
+    const uint64_t m = op_shard_stage(c, kind);
+    if (nrecords) *nrecords = m;
+  });
+}
+
+int rnndg_shard_export(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint32_t* dst_dev,
+                       uint64_t* key_dev, uint64_t* counts) {
+  return guarded(c, [&] {
+    need_graph(c);
+    if (!bounds || parts == 0 || !counts) throw ParamError("shard_export: bounds/counts required");
+    op_shard_export(c, bounds, parts, dst_dev, key_dev, counts);
+  });
+}
+
+int rnndg_shard_import(rnndg_ctx* c, int kind, const uint32_t* dst_dev, const uint64_t* key_dev,
+                       uint64_t nrecords, uint32_t R, rnndg_counts* partial, uint64_t* nstaged) {
+  return guarded(c, [&] {
+    need_graph(c);
+    if (kind < RNNDG_X_PENDING || kind > RNNDG_X_DELETE) throw ParamError("shard_import: bad kind");
+    if (kind == RNNDG_X_INEDGE && R < 1) throw ParamError("add_reverse_edges: R must be >= 1");
+    rnndg_counts cc{};
+    const uint64_t m = op_shard_import(c, kind, dst_dev, key_dev, nrecords, R, &cc);
+    if (partial) *partial = cc;
+    if (nstaged) *nstaged = m;
+  });
+}
+
+int rnndg_shard_out_prune(rnndg_ctx* c, uint32_t R) {
+  return guarded(c, [&] {
+    need_graph(c);
+    if (R < 1) throw ParamError("add_reverse_edges: R must be >= 1");
+    op_shard_out_prune(c, R);
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
   });
 }
 

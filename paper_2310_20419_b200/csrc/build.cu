@@ -26,6 +26,7 @@
 //   k_merge             merge post-scan list and new entries into the next CSR
 #define CCCL_IGNORE_DEPRECATED_API
 #include <cub/device/device_radix_sort.cuh>
+#include <vector>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
@@ -85,12 +86,13 @@ __device__ __forceinline__ uint32_t lower_bound(const uint64_t* a, uint32_t m, u
 // reference's S <= 64 branch and equivalent to its hash-set branch), then the
 // warp computes the S cached distances.
 template <bool kVec4>
-__global__ void k_random_init(uint64_t n, uint32_t S, uint64_t seed,
+__global__ void k_random_init(uint64_t n, uint64_t v0, uint64_t nv, uint32_t S, uint64_t seed,
                               const float* __restrict__ x, uint32_t d,
                               uint64_t* __restrict__ key) {
   const uint32_t lane = lane_id();
-  WARP_LOOP(u, n) {
-    uint64_t* out = key + u * S;
+  WARP_LOOP(ul, nv) {
+    const uint64_t u = v0 + ul;  // global id: the stream and the pivot are global
+    uint64_t* out = key + ul * S;
     if (lane == 0) {
       SplitMix64 rng(mix_seed(seed, u));
       const uint32_t domain = uint32_t(n - 1);  // exclude u
@@ -178,10 +180,14 @@ __global__ void k_label_step(uint64_t n, const uint64_t* __restrict__ off,
                              const uint32_t* __restrict__ cnt,
                              const uint64_t* __restrict__ key,
                              const uint32_t* __restrict__ lab_in,
-                             uint32_t* __restrict__ lab_out) {
+                             uint32_t* __restrict__ lab_out, int identity) {
   const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (u >= n) return;
   uint32_t m = lab_in ? lab_in[u] : uint32_t(u);
+  if (identity) {
+    lab_out[u] = uint32_t(u);
+    return;
+  }
   const uint64_t b = off[u];
   const uint32_t U = cnt[u];
   for (uint32_t j = 0; j < U; ++j) {
@@ -418,6 +424,134 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// ------------------------------------------------------------ sharding
+// Records exchanged between vertex owners are (dst, key)
+// pairs: dst a global vertex id, key an entry key addressed to dst's list.
+
+// redirects emitted by the scan (slot-indexed) -> compact records
+__global__ void k_pend_records(uint64_t span, const uint32_t* __restrict__ pend_src,
+                               const uint64_t* __restrict__ pend_key,
+                               unsigned long long* __restrict__ cursor,
+                               uint32_t* __restrict__ rdst, uint64_t* __restrict__ rkey) {
+  for (uint64_t e = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; e < span;
+       e += uint64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = pend_src[e];
+    if (s == kNone) continue;
+    const uint64_t at = atomicAdd(cursor, 1ull);
+    rdst[at] = s;
+    rkey[at] = pend_key[e];
+  }
+}
+
+// mode 0: reverse proposals (target, (dist, src, fresh)); mode 1: in-edges
+// (target, (dist, src, 0)) -- src global
+__global__ void __launch_bounds__(kBlock)
+    k_edge_records(uint64_t nv, uint64_t v0, const uint64_t* __restrict__ off,
+                   const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ key,
+                   unsigned long long* __restrict__ cursor, uint32_t* __restrict__ rdst,
+                   uint64_t* __restrict__ rkey, int mode) {
+  const uint32_t lane = lane_id();
+  WARP_LOOP(u, nv) {
+    const uint64_t b = off[u];
+    const uint32_t U = cnt[u];
+    uint64_t at = 0;
+    if (lane == 0 && U) at = atomicAdd(cursor, (unsigned long long)U);
+    at = __shfl_sync(0xffffffffu, at, 0);
+    for (uint32_t j = lane; j < U; j += 32) {
+      const uint64_t k = key[b + j];
+      rdst[at + j] = key_id(k);
+      rkey[at + j] = make_key(key_dist(k), uint32_t(v0 + u), mode == 0 ? 1u : 0u);
+    }
+  }
+}
+
+// received records -> per-owned-vertex buckets
+__global__ void k_rec_count(uint64_t nr, uint64_t v0, const uint32_t* __restrict__ rdst,
+                            unsigned long long* __restrict__ bcnt) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nr;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    atomicAdd(&bcnt[rdst[i] - v0], 1ull);
+}
+
+__global__ void k_rec_scatter(uint64_t nr, uint64_t v0, const uint32_t* __restrict__ rdst,
+                              const uint64_t* __restrict__ rkey,
+                              const uint64_t* __restrict__ boff,
+                              unsigned long long* __restrict__ bcur, uint64_t* __restrict__ bkey) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nr;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t u = rdst[i] - v0;
+    bkey[boff[u] + atomicAdd(&bcur[u], 1ull)] = rkey[i];
+  }
+}
+
+// in_prune at the target's owner: bucket sorted by (dist, source); ranks >= R
+// become deletion records (source, (dist, target, 0))
+__global__ void __launch_bounds__(kBlock)
+    k_inedge_select(uint64_t nv, uint64_t v0, const uint64_t* __restrict__ boff,
+                    const uint64_t* __restrict__ bkey, uint32_t R,
+                    unsigned long long* __restrict__ cursor, uint32_t* __restrict__ rdst,
+                    uint64_t* __restrict__ rkey) {
+  const uint32_t lane = lane_id();
+  WARP_LOOP(t, nv) {
+    const uint64_t b0 = boff[t], b1 = boff[t + 1];
+    if (b1 - b0 <= R) continue;
+    const uint64_t m = b1 - b0 - R;
+    uint64_t at = 0;
+    if (lane == 0) at = atomicAdd(cursor, (unsigned long long)m);
+    at = __shfl_sync(0xffffffffu, at, 0);
+    for (uint64_t r = lane; r < m; r += 32) {
+      const uint64_t k = bkey[b0 + R + r];
+      rdst[at + r] = key_id(k);
+      rkey[at + r] = make_key(key_dist(k), uint32_t(v0 + t), 0u);
+    }
+  }
+}
+
+// deletion records at the source's owner: locate the (dist, target) entry.
+// Positions are resolved for every record before any tombstone is written
+// (a tombstone inside a sorted list would break concurrent binary searches).
+__global__ void k_rec_locate(uint64_t nr, uint64_t v0, const uint32_t* __restrict__ rdst,
+                             const uint64_t* __restrict__ rkey, const uint64_t* __restrict__ off,
+                             const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ key,
+                             uint64_t* __restrict__ slot) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nr;
+       i += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t u = rdst[i] - v0;
+    const uint64_t* P = key + off[u];
+    const uint64_t k = rkey[i] & ~1ull;
+    const uint32_t pos = lower_bound(P, cnt[u], k);
+    slot[i] = (pos < cnt[u] && (P[pos] >> 1) == (k >> 1)) ? off[u] + pos : ~0ull;
+  }
+}
+
+__global__ void k_tomb_slots(uint64_t nr, const uint64_t* __restrict__ slot,
+                             uint64_t* __restrict__ key) {
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nr;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    if (slot[i] != ~0ull) key[slot[i]] = kTomb;
+}
+
+// per-destination-part counts of records sorted by dst: counts[p] = number of
+// dst in [bounds[p], bounds[p+1])
+__global__ void k_part_counts(uint64_t nr, const uint32_t* __restrict__ rdst,
+                              const uint64_t* __restrict__ bounds, uint32_t parts,
+                              unsigned long long* __restrict__ counts) {
+  const uint32_t p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= parts) return;
+  auto lb = [&](uint64_t v) {
+    uint64_t lo = 0, hi = nr;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (rdst[mid] < v)
+        lo = mid + 1;
+      else
+        hi = mid;
+    }
+    return lo;
+  };
+  counts[p] = lb(bounds[p + 1]) - lb(bounds[p]);
+}
+
 #undef WARP_LOOP
 
 // ------------------------------------------------------------- host glue
@@ -506,7 +640,7 @@ float elapsed_ms(cudaEvent_t a, cudaEvent_t b) {
 }
 
 void ensure_scratch(rnndg_ctx* c) {
-  const uint64_t n = c->n, span = c->span ? c->span : 1;
+  const uint64_t n = c->nv, span = c->span ? c->span : 1;
   c->active.ensure(n);
   c->act_list.ensure(2 * n);
   c->post_cnt.ensure(n + 1);
@@ -534,13 +668,13 @@ void ensure_scratch(rnndg_ctx* c) {
 // Sort each bucket [boff[u], boff[u+1]) of bkey into bkey_s.
 void sort_buckets(rnndg_ctx* c, uint64_t total) {
   if (total == 0) return;
-  seg_sort_keys(c, c->bkey.p, c->bkey_s.p, total, c->n, c->boff.p, c->boff.p + 1);
+  seg_sort_keys(c, c->bkey.p, c->bkey_s.p, total, c->nv, c->boff.p, c->boff.p + 1);
 }
 
 // Build graph B = merge(current lists with post_cnt, sorted buckets) and make
 // it the current graph.  New counts must be in c->cnt_b.
 void merge_and_swap(rnndg_ctx* c, const uint32_t* post_cnt) {
-  const uint64_t n = c->n;
+  const uint64_t n = c->nv;
   c->off_b.ensure(n + 1);
   scan_u32(c, c->cnt_b.p, c->off_b.p, n);
   const uint64_t total = read_u64(c, c->off_b.p + n);
@@ -556,14 +690,19 @@ void merge_and_swap(rnndg_ctx* c, const uint32_t* post_cnt) {
 // Locality order of the short active lists into c->act_small; count into
 // work[2] (read by the scan kernel).
 void locality_order(rnndg_ctx* c) {
-  const uint64_t n = c->n;
+  const uint64_t n = c->nv;
+  if (n == 0) {
+    zero(c, c->work.p + 2, 1);
+    return;
+  }
   uint32_t* la = c->label.p;
   uint32_t* lb = c->label.p + n;
+  // a shard's lists point at vertices it does not own: order by index there
   RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
-               nullptr, la);
-  for (int r = 1; r < kLabelRounds; ++r) {
+               nullptr, la, int(c->partitioned));
+  for (int r = 1; r < kLabelRounds && !c->partitioned; ++r) {
     RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
-                 la, lb);
+                 la, lb, 0);
     std::swap(la, lb);
   }
   uint64_t* ok = c->okey.p;
@@ -596,29 +735,32 @@ int sm_count(rnndg_ctx* c) {
 }
 
 void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
-  const uint64_t n = c->n;
+  const uint64_t n = c->n, nv = c->nv;
   if (n < 2) throw ParamError("random_init: need at least 2 vectors");
   if (S < 1 || S > n - 1) throw ParamError("random_init: S out of [1, n-1]");
-  c->span = n * S;
-  c->off.ensure(n + 1);
-  c->cnt.ensure(n + 1);
-  c->key.ensure(c->span);
-  RNNDG_LAUNCH(c, k_fill_offsets, grid_for(n + 1, 256), 256, 0, n, S, c->off.p, c->cnt.p);
-  if (c->d % 4 == 0)
-    RNNDG_LAUNCH(c, k_random_init<true>, warp_grid(c, n), kBlock, 0, n, S, seed, c->x, c->d,
-                 c->key.p);
-  else
-    RNNDG_LAUNCH(c, k_random_init<false>, warp_grid(c, n), kBlock, 0, n, S, seed, c->x, c->d,
-                 c->key.p);
+  c->span = nv * S;
+  c->off.ensure(nv + 1);
+  c->cnt.ensure(nv + 1);
+  c->key.ensure(c->span ? c->span : 1);
+  RNNDG_LAUNCH(c, k_fill_offsets, grid_for(nv + 1, 256), 256, 0, nv, S, c->off.p, c->cnt.p);
+  if (nv) {
+    if (c->d % 4 == 0)
+      RNNDG_LAUNCH(c, k_random_init<true>, warp_grid(c, nv), kBlock, 0, n, c->v0, nv, S, seed,
+                   c->x, c->d, c->key.p);
+    else
+      RNNDG_LAUNCH(c, k_random_init<false>, warp_grid(c, nv), kBlock, 0, n, c->v0, nv, S, seed,
+                   c->x, c->d, c->key.p);
+  }
   c->has_graph = true;
   c->has_distances = true;
   c->exact_dists = true;
   op_sort_lists(c);  // establish the sorted-list invariant
 }
 
-void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_sort,
-                    double* t_apply, uint64_t* touched, uint64_t* active_entries) {
-  const uint64_t n = c->n;
+// Scan phase of a pass: counters zeroed, active vertices marked, locality
+// order, distance stage.  Redirects end up in pend_src/pend_key by slot.
+void op_scan_phase(rnndg_ctx* c) {
+  const uint64_t n = c->nv;
   ensure_scratch(c);
   unsigned long long* ctr = c->counters.p;
   zero(c, ctr, kNumCounters);
@@ -628,12 +770,20 @@ void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_s
   zero(c, c->bcnt.p, n + 1);
   zero(c, c->bcur.p, n);
   RNNDG_CUDA(cudaEventRecord(c->ev[0], c->stream));
-  RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
-               c->active.p, c->act_list.p, c->post_cnt.p, ctr);
+  if (n)
+    RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
+                 c->active.p, c->act_list.p, c->post_cnt.p, ctr);
   locality_order(c);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
   launch_scan(c, c->work.p);
   RNNDG_CUDA(cudaEventRecord(c->ev[2], c->stream));
+}
+
+// Apply phase of a single-context pass: bucket the redirects by source,
+// append-if-absent, merge into the next CSR.
+void op_apply_local(rnndg_ctx* c) {
+  const uint64_t n = c->nv;
+  unsigned long long* ctr = c->counters.p;
   scan_u64(c, c->bcnt.p, c->boff.p, n);
   RNNDG_LAUNCH(c, k_pend_scatter, grid_for(c->span, 256, 148 * 64), 256, 0, c->span,
                c->pend_src.p, c->pend_key.p, c->boff.p, c->bcur.p, c->bkey.p);
@@ -642,9 +792,13 @@ void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_s
                c->post_cnt.p, c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, ctr, 1,
                int(c->exact_dists));
   merge_and_swap(c, c->post_cnt.p);
+}
+
+void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_sort,
+                      double* t_apply, uint64_t* touched, uint64_t* active_entries) {
   RNNDG_CUDA(cudaEventRecord(c->ev[3], c->stream));
   unsigned long long h[kNumCounters];
-  RNNDG_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaMemcpyAsync(h, c->counters.p, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
   RNNDG_CUDA(cudaStreamSynchronize(c->stream));
   if (out) {
     out->removed = h[kRemoved];
@@ -666,14 +820,21 @@ void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_s
                  elapsed_ms(c->ev[1], c->ev[2]), elapsed_ms(c->ev[2], c->ev[3]));
 }
 
+void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_sort,
+                    double* t_apply, uint64_t* touched, uint64_t* active_entries) {
+  op_scan_phase(c);
+  op_apply_local(c);
+  op_read_counters(c, out, t_scan, t_sort, t_apply, touched, active_entries);
+}
+
 namespace {
 
 void out_prune(rnndg_ctx* c, uint32_t R) {
-  RNNDG_LAUNCH(c, k_out_trunc, grid_for(c->n, 256), 256, 0, c->n, c->cnt.p, R);
+  RNNDG_LAUNCH(c, k_out_trunc, grid_for(c->nv, 256), 256, 0, c->nv, c->cnt.p, R);
 }
 
 void in_prune(rnndg_ctx* c, uint32_t R) {
-  const uint64_t n = c->n;
+  const uint64_t n = c->nv;
   zero(c, c->bcnt.p, n + 1);
   zero(c, c->bcur.p, n);
   RNNDG_LAUNCH(c, k_count_targets, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
@@ -711,7 +872,7 @@ void in_prune(rnndg_ctx* c, uint32_t R) {
 void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
   if (R < 1) throw ParamError("add_reverse_edges: R must be >= 1");
   if (!c->has_distances) throw ParamError("add_reverse_edges: graph has no distances");
-  const uint64_t n = c->n;
+  const uint64_t n = c->nv;
   ensure_scratch(c);
   // 1. reversals bucketed by their source (= target of the forward edge)
   zero(c, c->bcnt.p, n + 1);
@@ -744,12 +905,168 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
 }
 
 void op_sort_lists(rnndg_ctx* c) {
-  const uint64_t n = c->n;
+  const uint64_t n = c->nv;
   ensure_scratch(c);
   RNNDG_LAUNCH(c, k_seg_end, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, nullptr, 0u,
                c->seg_end.p);
   seg_sort_keys(c, c->key.p, c->key_s.p, c->span, n, c->off.p, c->seg_end.p);
   c->key.swap(c->key_s);
+}
+
+// ------------------------------------------------------- sharding ops
+void op_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end) {
+  if (v_begin > v_end || v_end > c->n) throw ParamError("set_partition: bad vertex range");
+  c->v0 = v_begin;
+  c->nv = v_end - v_begin;
+  c->partitioned = true;
+  c->has_graph = false;
+}
+
+uint64_t records_staged(rnndg_ctx* c) {
+  unsigned long long h = 0;
+  RNNDG_CUDA(cudaMemcpyAsync(&h, c->rec_cursor.p, 8, cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  c->rec_n = h;
+  return h;
+}
+
+void ensure_records(rnndg_ctx* c, uint64_t cap) {
+  c->rec_dst.ensure(cap ? cap : 1);
+  c->rec_key.ensure(cap ? cap : 1);
+  c->rec_dst2.ensure(cap ? cap : 1);
+  c->rec_key2.ensure(cap ? cap : 1);
+  c->rec_cursor.ensure(1);
+  zero(c, c->rec_cursor.p, 1);
+}
+
+// one pass's scan on the owned lists; redirects staged as records
+uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial, uint64_t* touched,
+                       uint64_t* active_entries) {
+  op_scan_phase(c);
+  ensure_records(c, c->span);
+  if (c->span)
+    RNNDG_LAUNCH(c, k_pend_records, grid_for(c->span, 256, 148 * 64), 256, 0, c->span,
+                 c->pend_src.p, c->pend_key.p, c->rec_cursor.p, c->rec_dst.p, c->rec_key.p);
+  // counters of the scan phase (removed, flag_skips, pair_checks)
+  op_read_counters(c, partial, nullptr, nullptr, nullptr, touched, active_entries);
+  return records_staged(c);
+}
+
+// stage reverse proposals (kind 1) or in-edges (kind 2) of the owned lists
+uint64_t op_shard_stage(rnndg_ctx* c, int kind) {
+  uint64_t m = 0;
+  {
+    std::vector<uint32_t> cnt(c->nv);
+    if (c->nv)
+      RNNDG_CUDA(cudaMemcpyAsync(cnt.data(), c->cnt.p, c->nv * 4, cudaMemcpyDeviceToHost, c->stream));
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+    for (uint32_t v : cnt) m += v;
+  }
+  ensure_records(c, m);
+  if (c->nv)
+    RNNDG_LAUNCH(c, k_edge_records, warp_grid(c, c->nv), kBlock, 0, c->nv, c->v0, c->off.p,
+                 c->cnt.p, c->key.p, c->rec_cursor.p, c->rec_dst.p, c->rec_key.p,
+                 kind == RNNDG_X_PROPOSAL ? 0 : 1);
+  return records_staged(c);
+}
+
+// staged records sorted by destination into caller device buffers, with the
+// count per destination part ([bounds[p], bounds[p+1]) ids)
+void op_shard_export(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint32_t* dst_dev,
+                     uint64_t* key_dev, uint64_t* counts) {
+  const uint64_t nr = c->rec_n;
+  if (nr) {
+    if (nr > uint64_t(INT32_MAX)) throw CudaError("export: too many records");
+    size_t bytes = 0;
+    RNNDG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, c->rec_dst.p, c->rec_dst2.p,
+                                               c->rec_key.p, c->rec_key2.p, int(nr), 0, 32,
+                                               c->stream));
+    RNNDG_CUDA(cub::DeviceRadixSort::SortPairs(cub_temp(c, bytes), bytes, c->rec_dst.p,
+                                               c->rec_dst2.p, c->rec_key.p, c->rec_key2.p, int(nr),
+                                               0, 32, c->stream));
+    c->launches += 4;
+    RNNDG_CUDA(cudaMemcpyAsync(dst_dev, c->rec_dst2.p, nr * 4, cudaMemcpyDeviceToDevice, c->stream));
+    RNNDG_CUDA(cudaMemcpyAsync(key_dev, c->rec_key2.p, nr * 8, cudaMemcpyDeviceToDevice, c->stream));
+  }
+  c->part_bounds.ensure(parts + 1);
+  c->part_counts.ensure(parts);
+  RNNDG_CUDA(cudaMemcpyAsync(c->part_bounds.p, bounds, (parts + 1) * 8, cudaMemcpyHostToDevice,
+                             c->stream));
+  RNNDG_LAUNCH(c, k_part_counts, (parts + 127) / 128, 128, 0, nr, c->rec_dst2.p,
+               c->part_bounds.p, parts, c->part_counts.p);
+  RNNDG_CUDA(cudaMemcpyAsync(counts, c->part_counts.p, parts * 8, cudaMemcpyDeviceToHost,
+                             c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// received records -> owned lists.  kind: redirects (append-if-absent,
+// counted as inserted), reverse proposals (append-if-absent), in-edges
+// (select deletions, staged for export), deletions (apply).
+uint64_t op_shard_import(rnndg_ctx* c, int kind, const uint32_t* dst_dev, const uint64_t* key_dev,
+                         uint64_t nr, uint32_t R, rnndg_counts* partial) {
+  const uint64_t n = c->nv;
+  ensure_scratch(c);
+  if (kind == RNNDG_X_DELETE) {
+    if (nr) {
+      c->rec_key2.ensure(nr);
+      RNNDG_LAUNCH(c, k_rec_locate, grid_for(nr, 256, 148 * 64), 256, 0, nr, c->v0, dst_dev,
+                   key_dev, c->off.p, c->cnt.p, c->key.p, c->rec_key2.p);
+      RNNDG_LAUNCH(c, k_tomb_slots, grid_for(nr, 256, 148 * 64), 256, 0, nr, c->rec_key2.p,
+                   c->key.p);
+    }
+    RNNDG_LAUNCH(c, k_count_live, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
+                 c->cnt_b.p);
+    c->off_b.ensure(n + 1);
+    scan_u32(c, c->cnt_b.p, c->off_b.p, n);
+    const uint64_t total = read_u64(c, c->off_b.p + n);
+    c->key_b.ensure(total ? total : 1);
+    RNNDG_LAUNCH(c, k_compact, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
+                 c->off_b.p, c->key_b.p);
+    c->off.swap(c->off_b);
+    c->key.swap(c->key_b);
+    c->cnt.swap(c->cnt_b);
+    c->span = total;
+    return 0;
+  }
+  // bucket by owned destination
+  zero(c, c->bcnt.p, n + 1);
+  zero(c, c->bcur.p, n);
+  c->bkey.ensure(nr ? nr : 1);
+  c->bkey_s.ensure(nr ? nr : 1);
+  c->bflag.ensure(nr ? nr : 1);
+  c->brank.ensure(nr ? nr : 1);
+  if (nr)
+    RNNDG_LAUNCH(c, k_rec_count, grid_for(nr, 256, 148 * 64), 256, 0, nr, c->v0, dst_dev, c->bcnt.p);
+  scan_u64(c, c->bcnt.p, c->boff.p, n);
+  if (nr)
+    RNNDG_LAUNCH(c, k_rec_scatter, grid_for(nr, 256, 148 * 64), 256, 0, nr, c->v0, dst_dev,
+                 key_dev, c->boff.p, c->bcur.p, c->bkey.p);
+  sort_buckets(c, nr);
+  if (kind == RNNDG_X_INEDGE) {
+    ensure_records(c, nr);
+    RNNDG_LAUNCH(c, k_inedge_select, warp_grid(c, n), kBlock, 0, n, c->v0, c->boff.p,
+                 c->bkey_s.p, R, c->rec_cursor.p, c->rec_dst.p, c->rec_key.p);
+    return records_staged(c);
+  }
+  // redirects / proposals: append-if-absent into the (post-scan) lists
+  unsigned long long* ctr = c->counters.p;
+  zero(c, ctr, kNumCounters);
+  const uint32_t* post = kind == RNNDG_X_PENDING ? c->post_cnt.p : c->cnt.p;
+  RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p, post,
+               c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, ctr,
+               kind == RNNDG_X_PENDING ? 1 : 0, int(c->exact_dists));
+  merge_and_swap(c, post);
+  if (partial) {
+    unsigned long long h[kNumCounters];
+    RNNDG_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+    *partial = rnndg_counts{0, h[kInserted], 0, 0};
+  }
+  return 0;
+}
+
+void op_shard_out_prune(rnndg_ctx* c, uint32_t R) {
+  if (c->nv) RNNDG_LAUNCH(c, k_out_trunc, grid_for(c->nv, 256), 256, 0, c->nv, c->cnt.p, R);
 }
 
 }  // namespace rnndg

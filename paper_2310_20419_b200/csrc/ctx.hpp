@@ -90,8 +90,12 @@ struct rnndg_ctx {
   // VectorStore (vector_store.hpp:12-20), row-major n x d fp32
   rnndg::DevBuf<float> x_own;
   const float* x = nullptr;
-  uint64_t n = 0;
+  uint64_t n = 0;  // rows of the store (global vertex count)
   uint32_t d = 0;
+  // lists held by this context: vertices [v0, v0 + nv) (SURVEY 8(e) ownership
+  // ranges; nv = n, v0 = 0 unless rnndg_set_partition was called)
+  uint64_t v0 = 0, nv = 0;
+  bool partitioned = false;
 
   // Graph "A": lists at key[off[u] .. off[u] + cnt[u]).  off is monotone and
   // may leave gaps between lists (capacity layout); span = off[n].
@@ -116,6 +120,11 @@ struct rnndg_ctx {
   rnndg::DevBuf<unsigned long long> counters;
   rnndg::DevBuf<unsigned int> work;
   rnndg::DevBuf<uint32_t> kpos_g;  // scan scratch for lists > kScanUcap
+  // sharding: staged (dst, key) records, per-part counts
+  rnndg::DevBuf<uint32_t> rec_dst, rec_dst2;
+  rnndg::DevBuf<uint64_t> rec_key, rec_key2, part_bounds;
+  rnndg::DevBuf<unsigned long long> rec_cursor, part_counts;
+  uint64_t rec_n = 0;
   // chain-blocked copy of the store for the distance stage (scan.cu)
   rnndg::DevBuf<float> xp;
   const float* xp_src = nullptr;
@@ -150,8 +159,21 @@ void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed);
 void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan,
                     double* t_sort, double* t_apply, uint64_t* touched,
                     uint64_t* active_entries);
+void op_scan_phase(rnndg_ctx* c);
+void op_apply_local(rnndg_ctx* c);
+void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_sort,
+                      double* t_apply, uint64_t* touched, uint64_t* active_entries);
 void op_reverse(rnndg_ctx* c, uint32_t R, int order);
 void op_sort_lists(rnndg_ctx* c);
+void op_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end);
+uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial, uint64_t* touched,
+                       uint64_t* active_entries);
+uint64_t op_shard_stage(rnndg_ctx* c, int kind);
+void op_shard_export(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint32_t* dst_dev,
+                     uint64_t* key_dev, uint64_t* counts);
+uint64_t op_shard_import(rnndg_ctx* c, int kind, const uint32_t* dst_dev, const uint64_t* key_dev,
+                         uint64_t nr, uint32_t R, rnndg_counts* partial);
+void op_shard_out_prune(rnndg_ctx* c, uint32_t R);
 int sm_count(rnndg_ctx* c);
 
 // eval.cu

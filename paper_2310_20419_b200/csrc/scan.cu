@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
             const uint32_t w_id = key_id(wk);
             g.pend_src[base + q] = w_id;
             g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
-            atomicAdd(&g.bcnt[w_id], 1ull);
+            if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
           }
         }
         uint32_t nstay;
@@ -587,7 +587,7 @@ __global__ void __launch_bounds__(32 * W) k_scan_sliced(ScanArgs g) {
             const uint32_t w_id = key_id(wk);
             g.pend_src[base + q] = w_id;
             g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
-            atomicAdd(&g.bcnt[w_id], 1ull);
+            if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
           }
         }
         uint32_t nstay;
@@ -812,7 +812,7 @@ __global__ void __launch_bounds__(32 * W) k_scan_pull(ScanArgs g) {
                 const uint32_t w_id = key_id(wk);
                 g.pend_src[base + vp] = w_id;
                 g.pend_key[base + vp] = make_key(dvw, key_id(vk), 1u);
-                atomicAdd(&g.bcnt[w_id], 1ull);
+                if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
                 break;
               }
             }
@@ -859,7 +859,7 @@ __global__ void __launch_bounds__(32 * W) k_scan_pull(ScanArgs g) {
                   const uint32_t w_id = key_id(wk);
                   g.pend_src[base + vp] = w_id;
                   g.pend_key[base + vp] = make_key(dvw, key_id(vk), 1u);
-                  atomicAdd(&g.bcnt[w_id], 1ull);
+                  if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
                   break;
                 }
               }
@@ -933,7 +933,7 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   a.act_small = c->act_small.p;
   a.nsmall = reinterpret_cast<const int*>(work + 2);
   a.act_list = c->act_list.p;
-  a.n = c->n;
+  a.n = c->nv;  // long lists are queued at act_list[nv ..)
   a.ctr_in = c->counters.p;
   a.work = work;
   a.off = c->off.p;
@@ -945,7 +945,7 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   a.post_cnt = c->post_cnt.p;
   a.pend_src = c->pend_src.p;
   a.pend_key = c->pend_key.p;
-  a.bcnt = c->bcnt.p;
+  a.bcnt = c->partitioned ? nullptr : c->bcnt.p;
   a.ctr = c->counters.p;
   // row slots: stride padded to an odd multiple of 16 B (quads of two CTAs'
   // rows land in different bank groups); ~100 KB per CTA for long rows
