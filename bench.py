@@ -187,6 +187,64 @@ def cpu_baseline(cfg, sample):
             "sample": f"C oracle build (1 thread) on the first {n} rows of {cfg.name}"}
 
 
+def run_sharded(args, rank, world, local):
+    """N > 1: the same workload, vertex ownership split over the ranks
+    (SURVEY 8(e)); redirects / reverse proposals / in-edges / deletions are
+    exchanged with NCCL all-to-all.  Total work is fixed: strong scaling."""
+    import torch
+    import torch.distributed as dist
+    from paper_2310_20419_b200 import datagen
+    from paper_2310_20419_b200 import sharded as SH
+    cfg = datagen.CONFIGS[args.config]
+    n = args.n or cfg.n
+    data = store_rows(cfg, n)
+    b = SH.ownership_bounds(n, world)
+    eng = SH.DeviceShard(data, b[rank], b[rank + 1], device=local)
+    tr = SH.TorchDistTransport()
+    p = dict(S=20, R=96, T1=4, T2=15, seed=42)
+
+    def one_build():
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        st = SH.sharded_build([eng], tr, n, world, **p)
+        e1.record()
+        torch.cuda.synchronize()
+        return st, e0.elapsed_time(e1) * 1e-3
+
+    for _ in range(args.warmup):
+        one_build()
+    dist.barrier()
+    secs, checks = 0.0, 0
+    with ClockSampler(local) as clk:
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            st, dt = one_build()
+            secs += dt
+            checks += int(st.edits[3])  # already summed over ranks
+        wall = time.perf_counter() - t0
+    t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_secs = float(t[0])
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": checks / max_secs, "unit": "dist-evals/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * max_secs / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (seeded generator, csrc/datagen.cpp; stands in for GIST1M)",
+            "config": {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96, "T1": 4,
+                       "T2": 15, "parallelism": f"vertex-sharded x{world} (NCCL all-to-all)",
+                       "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},
+            "build_seconds": max_secs / args.steps, "wall_seconds_timed": wall,
+            "pair_checks_per_build": checks // args.steps,
+            "roofline": None, "cpu_baseline": None, "e2e": None,
+            "gpu_launches": None, "clocks": clk.summary(),
+        }
+        print(json.dumps(line))
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
@@ -199,6 +257,9 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        run_sharded(args, rank, world, local)
+        dist.destroy_process_group()
+        return
     from paper_2310_20419_b200 import _lib, datagen
     from paper_2310_20419_b200 import rnnd as R
 
