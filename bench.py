@@ -306,16 +306,21 @@ def main():
     alg_bytes = 4.0 * cfg.d * st0.touched + 24.0 * st0.active_entries
     achieved = alg_bytes / st0.scan_seconds / 1e9
     peak, peak_src = hbm_peak()
-    traffic = None
-    tpath = os.path.join(ROOT, "profiles", "scan_traffic.json")
-    if os.path.exists(tpath):
+    # DRAM traffic of one distance-stage launch, from the committed ncu
+    # --set full capture of this workload (per launch; algorithmic bytes of
+    # the same pass alongside)
+    traffic, traffic_alg, traffic_src = None, None, None
+    import glob
+    for tpath in sorted(glob.glob(os.path.join(ROOT, "profiles", "*scan_traffic*.json"))):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            if tj.get("config") == cfg.name:
-                traffic = tj.get("traffic_bytes_per_build")
         except Exception:
-            traffic = None
+            continue
+        if tj.get("config") == cfg.name and n == cfg.n:
+            traffic = tj.get("dram_bytes_per_launch")
+            traffic_alg = tj.get("algorithmic_bytes_same_pass")
+            traffic_src = os.path.relpath(tpath, ROOT) + ": " + tj.get("kernel", "")
 
     # end to end through the C ABI with host buffers (H2D, build, D2H)
     e2e = None
@@ -380,6 +385,8 @@ def main():
                               "apply": st0.apply_seconds, "reverse": st0.reverse_seconds},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic,
+                         "traffic_algorithmic_bytes_same_launch": traffic_alg,
+                         "traffic_source": traffic_src,
                          "kernel": "k_scan (distance stage)",
                          "algorithmic_bytes_per_build": alg_bytes,
                          "touched": st0.touched, "active_entries": st0.active_entries,
