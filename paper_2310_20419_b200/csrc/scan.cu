@@ -286,11 +286,12 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
   constexpr uint32_t kCap = kLong ? 1 : kScanUcap;
   __shared__ uint64_t keys_sh[kCap];
   __shared__ uint32_t alive_sh[kCap];
-  __shared__ uint32_t tq[NT];   // task: list position of the candidate
-  __shared__ uint64_t tk[NT];   //       its key
-  __shared__ float tres[NT];    //       its distance to the kept entry
+  __shared__ uint32_t tq[2 * NT];  // task: list position of the candidate
+  __shared__ uint64_t tk[2 * NT];  //       its key
+  __shared__ float tres[2 * NT];   //       its distance to the kept entry
+  __shared__ uint8_t tsel[2 * NT]; //       which kept entry (0: w1, 1: w2)
   __shared__ uint32_t wcnt[W];
-  __shared__ uint32_t s_a;
+  __shared__ uint32_t s_a, s_w2kept;
   __shared__ uint64_t bar;
   const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
   const uint32_t quad = lane >> 2, chain = lane & 3;
@@ -314,14 +315,12 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
     const uint32_t U = g.cnt[u];
     uint64_t* L = g.keys + base;
     uint8_t* T = g.touch + base;
-    // kLong: keys are read from L directly; the kept entry of a step is
-    // written to L[nk] with nk <= p < every alive position, so no alive key
-    // is overwritten
+    // kLong: keys are read from L directly; the kept entries of a step are
+    // written to L[nk..] with nk <= p < every alive position
     const uint64_t* K = kLong ? L : keys_sh;
     uint32_t* A = kLong ? g.alive_g + base : alive_sh;
     // kStage: the nearest min(U, nslots) rows go to shared-memory slots with
-    // one TMA bulk copy each (HBM read once per scanned vertex); the rest are
-    // read through L2, prefetched in bulk
+    // one TMA bulk copy each; the rest are read through L2 (bulk prefetch)
     const uint32_t nst = kStage ? (U < g.nslots ? U : g.nslots) : 0u;
     for (uint32_t j = tid; j < U; j += NT) {
       const uint64_t k = L[j];
@@ -347,30 +346,47 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
     };
     uint32_t na = U, nk = 0;
     while (na) {
-      // the first alive candidate is kept: every earlier kept entry has
-      // already been tested against it
-      const uint32_t p = A[0];
-      const uint64_t wk = K[p];
-      const bool wf = key_fresh(wk);
-      const float* xw = rowp(p, wk);
-      __syncthreads();  // all threads have read A[0] / K[p]
-      if (tid == 0) L[nk] = wk & ~1ull;  // flagged old (builder.cpp:68)
+      // Two push steps at once: w1 = first alive candidate (kept: every
+      // earlier kept entry has already been tested against it) and w2 = the
+      // second, provisionally kept.  Pairs with w2 are evaluated
+      // speculatively and counted only for candidates that survive w1, and
+      // only if w2 itself survives w1 -- exactly the reference's pairs.
+      const uint32_t p1 = A[0];
+      const uint64_t wk1 = K[p1];
+      const bool wf1 = key_fresh(wk1);
+      const float* xw1 = rowp(p1, wk1);
+      const bool two = na >= 2;
+      const uint32_t p2 = two ? A[1] : p1;
+      const uint64_t wk2 = K[p2];
+      const bool wf2 = key_fresh(wk2);
+      const float* xw2 = rowp(p2, wk2);
+      __syncthreads();  // all threads have read A[0..1] / K[p]
+      if (tid == 0) L[nk] = wk1 & ~1ull;  // flagged old (builder.cpp:68)
       ++nk;
       uint32_t nn = 0;  // survivors so far, compacted in place into A[0 ..)
+      bool w2kept = false;
       for (uint32_t b0 = 1; b0 < na; b0 += NT) {
         const uint32_t ai = b0 + tid;
         const bool valid = ai < na;
         const uint32_t q = valid ? A[ai] : 0u;
         const uint64_t vk = valid ? K[q] : 0ull;
-        const bool need = valid && (wf || key_fresh(vk));  // builder.cpp:53-56
-        skips += (valid && !need) ? 1 : 0;
-        uint32_t ntask;
-        const uint32_t t = block_rank<W>(need, wcnt, ntask);
-        if (need) {
-          tq[t] = q;
-          tk[t] = vk;
+        const bool vf = key_fresh(vk);
+        const bool need1 = valid && (wf1 || vf);  // builder.cpp:53-56
+        const bool need2 = valid && ai >= 2 && (wf2 || vf);
+        uint32_t n1, n2;
+        const uint32_t t1 = block_rank<W>(need1, wcnt, n1);
+        const uint32_t t2 = n1 + block_rank<W>(need2, wcnt, n2);
+        if (need1) {
+          tq[t1] = q;
+          tk[t1] = vk;
+          tsel[t1] = 0;
         }
-        checks += need ? 1 : 0;
+        if (need2) {
+          tq[t2] = q;
+          tk[t2] = vk;
+          tsel[t2] = 1;
+        }
+        const uint32_t ntask = n1 + n2;
         __syncthreads();
         for (uint32_t t0 = 0; t0 < ntask; t0 += 8 * W) {
           const uint32_t tw = t0 + 8 * wid;
@@ -379,33 +395,62 @@ __global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
           const bool has = ti < ntask;
           const uint32_t ts = has ? ti : tw;
           const float* xv = rowp(tq[ts], tk[ts]);
+          const float* xw = tsel[ts] ? xw2 : xw1;
           const float dist = kStage ? quad_l2_any(xv, xw, chain, row.nblk, row.ntail)
                                     : quad_l2(xv, xw, chain, row.nblk, row.ntail);
-          if (has && chain == 0) {
-            tres[ti] = dist;
-            T[tq[ti]] = 1;
-            T[p] = 1;
-          }
+          if (has && chain == 0) tres[ti] = dist;
         }
         __syncthreads();
-        bool gone = false;
-        if (need) {
-          const float dvw = tres[t];
+        // resolve w1 for every candidate; the fate of w2 (candidate ai == 1)
+        // is known in the first batch
+        bool gone = false, by2 = false;
+        float dvw = 0.f;
+        if (need1) {
+          dvw = tres[t1];
+          ++checks;
+          T[q] = 1;
+          T[p1] = 1;
           gone = key_dist(vk) >= dvw;
-          if (gone) {
-            ++removed;
-            const uint32_t w_id = key_id(wk);
-            g.pend_src[base + q] = w_id;
-            g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
-            if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
+        } else if (valid) {
+          ++skips;
+        }
+        if (ai == 1) s_w2kept = (valid && !gone) ? 1u : 0u;
+        __syncthreads();
+        w2kept = two && s_w2kept;
+        if (valid && !gone && ai >= 2 && w2kept) {
+          if (need2) {
+            const float d2 = tres[t2];
+            ++checks;
+            T[q] = 1;
+            T[p2] = 1;
+            if (key_dist(vk) >= d2) {
+              gone = true;
+              by2 = true;
+              dvw = d2;
+            }
+          } else {
+            ++skips;
           }
         }
+        if (gone) {
+          ++removed;
+          const uint32_t w_id = key_id(by2 ? wk2 : wk1);
+          g.pend_src[base + q] = w_id;
+          g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
+          if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
+        }
+        // survivors stay alive; a kept w2 leaves the alive list
+        const bool stay = valid && !gone && !(ai == 1 && w2kept);
         uint32_t nstay;
-        const uint32_t r = block_rank<W>(valid && !gone, wcnt, nstay);
+        const uint32_t r = block_rank<W>(stay, wcnt, nstay);
         // every thread of the batch has read its A[ai] (block_rank syncs)
-        if (valid && !gone) A[nn + r] = q;
+        if (stay) A[nn + r] = q;
         nn += nstay;
         __syncthreads();
+      }
+      if (w2kept) {
+        if (tid == 0) L[nk] = wk2 & ~1ull;
+        ++nk;
       }
       na = nn;
     }
