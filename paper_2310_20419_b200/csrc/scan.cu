@@ -24,7 +24,7 @@
 // lifetime, so fewer vertices are in flight and their rows stay in L2 between
 // push steps (ncu: a warp-per-vertex scan re-read rows from HBM at every step).
 //
-//   k_scan_block<4, false>   lists <= kScanUcap; keys + alive list in smem
+//   k_scan_block<2, false>   lists <= kScanUcap; keys + alive list in smem
 //   k_scan_block<32, true>   longer lists (hubs that collect redirects), on a
 //                            second stream concurrently
 #include <cstdio>
@@ -38,7 +38,8 @@ namespace rnndg {
 
 namespace {
 
-constexpr int kShortWarps = 4;   // one 128-thread CTA per short list
+constexpr int kShortWarps = 4;   // staged / sliced experiments: 128-thread CTAs
+constexpr int kPushWarps = 2;    // default push scan: one 64-thread CTA per short list
 constexpr int kLongWarps = 32;   // one 1024-thread CTA per long list
 
 // Chain-blocked row layout: element e < d4 = d - d % 4 lives at
@@ -279,7 +280,7 @@ __device__ __forceinline__ uint32_t block_rank(bool pred, uint32_t* wcnt, uint32
 // otherwise keys and alive list live in shared memory (queue act_small,
 // work[0]).
 template <int W, bool kLong, bool kStage>
-__global__ void __launch_bounds__(32 * W) k_scan_block(ScanArgs g) {
+__global__ void __launch_bounds__(32 * W, 1) k_scan_block(ScanArgs g) {
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   float* slots = reinterpret_cast<float*>(dyn_smem);
   constexpr uint32_t NT = 32 * W;
@@ -1033,11 +1034,24 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     const char* e = std::getenv("RNNDG_PULL_KB");
     return e ? std::atoi(e) : 0;
   }();
+  // warps per CTA of the push kernel (RNNDG_SHORT_W = 1 | 2 | 4 | 8).  Two
+  // warps with an unconstrained register budget (147 regs, 6 CTAs/SM) beat
+  // four warps (-6%) and register-capped variants with more CTAs per SM
+  // (profiles/README.md, r01 tuning).
+  static const int short_w = [] {
+    const char* e = std::getenv("RNNDG_SHORT_W");
+    const int v = e ? std::atoi(e) : kPushWarps;
+    return v == 1 || v == 2 || v == 4 || v == 8 ? v : kPushWarps;
+  }();
+  auto kpush = short_w == 1   ? k_scan_block<1, false, false>
+               : short_w == 2 ? k_scan_block<2, false, false>
+               : short_w == 4 ? k_scan_block<4, false, false>
+                              : k_scan_block<8, false, false>;
   auto kshort = stage ? k_scan_block<kShortWarps, false, true>
                       : (sliced ? k_scan_sliced<kShortWarps>
-                                : (push ? k_scan_block<kShortWarps, false, false>
+                                : (push ? kpush
                                         : (pull_w == 4 ? k_scan_pull<4> : k_scan_pull<8>)));
-  unsigned threads_short = 32 * (push || stage || sliced ? kShortWarps : pull_w);
+  unsigned threads_short = 32 * (stage || sliced ? kShortWarps : (push ? short_w : pull_w));
   if (!push && !stage && !sliced) {
     const size_t pbudget = pull_kb > 0 ? size_t(pull_kb) * 1024
                                        : (slot_bytes >= 2048 ? 150 * 1024 : 96 * 1024);
