@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_ROWS)
+    ap.add_argument("--sharded", action="store_true",
+                    help="use the vertex-sharded build even at N=1 (checks that path)")
     return ap.parse_args()
 
 
@@ -216,6 +218,8 @@ def run_sharded(args, rank, world, local):
     for _ in range(args.warmup):
         one_build()
     dist.barrier()
+    eng.totals(reset=True)
+    launches0 = eng.launches()
     secs, checks = 0.0, 0
     with ClockSampler(local) as clk:
         t0 = time.perf_counter()
@@ -224,10 +228,37 @@ def run_sharded(args, rank, world, local):
             secs += dt
             checks += int(st.edits[3])  # already summed over ranks
         wall = time.perf_counter() - t0
-    t = torch.tensor([secs], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_secs = float(t[0])
+    launches = eng.launches() - launches0
+    tot = eng.totals(reset=True)
+
+    # end to end: H2D of the store from pinned host memory, the sharded
+    # build, D2H of this rank's lists; max over ranks
+    pinned = torch.empty(data.shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = data
+    e2e_secs, d2h = 0.0, 0
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        dist.barrier()
+        t = time.perf_counter()
+        eng.load(pinned.numpy())
+        SH.sharded_build([eng], tr, n, world, **p)
+        part = eng.graph()
+        e2e_secs += time.perf_counter() - t
+        d2h = int(part.offsets.nbytes + 12 * len(part.ids))
+
+    vals = torch.tensor([secs, e2e_secs, tot["scan_seconds"], float(launches)],
+                        dtype=torch.float64, device="cuda")
+    dist.all_reduce(vals, op=dist.ReduceOp.MAX)
+    units = torch.tensor([float(tot["touched"]), float(tot["active_entries"]), float(d2h)],
+                         dtype=torch.float64, device="cuda")
+    dist.all_reduce(units, op=dist.ReduceOp.SUM)
+    max_secs, max_e2e, max_scan = float(vals[0]), float(vals[1]), float(vals[2])
     if rank == 0:
+        # roofline: algorithmic bytes of all shards' scans per GPU over the
+        # slowest rank's distance-stage time
+        alg = (4.0 * cfg.d * float(units[0]) + 24.0 * float(units[1])) / args.steps
+        achieved = alg / world / (max_scan / args.steps) / 1e9 if max_scan > 0 else 0.0
+        peak, peak_src = hbm_peak()
         line = {
             "metric": METRIC, "value": checks / max_secs, "unit": "dist-evals/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -239,8 +270,17 @@ def run_sharded(args, rank, world, local):
                        "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},
             "build_seconds": max_secs / args.steps, "wall_seconds_timed": wall,
             "pair_checks_per_build": checks // args.steps,
-            "roofline": None, "cpu_baseline": None, "e2e": None,
-            "gpu_launches": None, "clocks": clk.summary(),
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": None,
+                         "kernel": "k_scan (distance stage), per GPU, max-rank time",
+                         "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": {"value": checks / max_e2e, "unit": "dist-evals/s",
+                    "h2d_bytes_per_step": int(data.nbytes) * world,
+                    "d2h_bytes_per_step": int(units[2]),
+                    "seconds_per_step": max_e2e / args.steps},
+            "gpu_launches": int(vals[3]) * world,
+            "clocks": clk.summary(),
         }
         print(json.dumps(line))
 
@@ -254,8 +294,12 @@ def main():
 
     import torch
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 or args.sharded:
         import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        os.environ.setdefault("RANK", str(rank))
+        os.environ.setdefault("WORLD_SIZE", str(world))
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         run_sharded(args, rank, world, local)
         dist.destroy_process_group()
@@ -273,8 +317,6 @@ def main():
 
     def barrier():
         torch.cuda.synchronize()
-        if world > 1:
-            torch.distributed.barrier()
 
     for _ in range(args.warmup):
         R.build(store, params, device=dev)
@@ -292,14 +334,8 @@ def main():
     launches = dev.launches() - launches0
     dev_secs = sum(s.seconds for s in stats)
     checks = sum(s.edits.pair_checks for s in stats)
-    t_rank = torch.tensor([dev_secs, float(checks)], dtype=torch.float64, device="cuda")
-    if world > 1:
-        mx = t_rank.clone()
-        torch.distributed.all_reduce(mx[:1], op=torch.distributed.ReduceOp.MAX)
-        torch.distributed.all_reduce(t_rank[1:], op=torch.distributed.ReduceOp.SUM)
-        t_rank[0] = mx[0]
-    max_secs, all_checks = float(t_rank[0]), float(t_rank[1])
-    value = all_checks / max_secs
+    max_secs = dev_secs
+    value = checks / max_secs
 
     # roofline of the distance stage: B = 4 d T + 24 A bytes
     st0 = stats[-1]
@@ -323,29 +359,26 @@ def main():
             traffic_src = os.path.relpath(tpath, ROOT) + ": " + tj.get("kernel", "")
 
     # end to end through the C ABI with host buffers (H2D, build, D2H)
-    e2e = None
-    if rank == 0 or world > 1:
-        pinned = torch.empty(data.shape, dtype=torch.float32, pin_memory=True)
-        pinned.numpy()[:] = data
-        pstore = R.VectorStore(pinned.numpy())
-        e2e_secs, e2e_checks, d2h = 0.0, 0, 0
-        for _ in range(args.steps):
-            edev = dev
-            torch.cuda.synchronize()
-            t = time.perf_counter()
-            edev.set_data(pstore)  # H2D
-            st = R.BuildStats()
-            g = R.build(pstore, params, st, device=edev)
-            csr = edev.get_graph()  # D2H
-            e2e_secs += time.perf_counter() - t
-            e2e_checks += st.edits.pair_checks
-            d2h = int(csr.offsets.nbytes + 12 * len(csr.ids))
-        e2e = {"value": e2e_checks / e2e_secs, "unit": "dist-evals/s",
-               "h2d_bytes_per_step": int(data.nbytes), "d2h_bytes_per_step": d2h,
-               "seconds_per_step": e2e_secs / args.steps}
+    pinned = torch.empty(data.shape, dtype=torch.float32, pin_memory=True)
+    pinned.numpy()[:] = data
+    pstore = R.VectorStore(pinned.numpy())
+    e2e_secs, e2e_checks, d2h = 0.0, 0, 0
+    for _ in range(args.steps):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        dev.set_data(pstore)  # H2D
+        st = R.BuildStats()
+        g = R.build(pstore, params, st, device=dev)
+        csr = dev.get_graph()  # D2H
+        e2e_secs += time.perf_counter() - t
+        e2e_checks += st.edits.pair_checks
+        d2h = int(csr.offsets.nbytes + 12 * len(csr.ids))
+    e2e = {"value": e2e_checks / e2e_secs, "unit": "dist-evals/s",
+           "h2d_bytes_per_step": int(data.nbytes), "d2h_bytes_per_step": d2h,
+           "seconds_per_step": e2e_secs / args.steps}
 
     recall = None
-    if rank == 0 and not args.no_recall:
+    if not args.no_recall:
         nq = min(cfg.nq, 1000)
         q = datagen.rows(cfg.cfg, cfg.seed, cfg.n, nq) if n == cfg.n else \
             datagen.rows(cfg.cfg, cfg.seed, n, nq)
@@ -365,41 +398,38 @@ def main():
         recall["max_out"] = deg.max_out
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if not args.no_cpu_baseline:
         cpu = cpu_baseline(cfg, args.cpu_sample)
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": "dist-evals/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1e3 * max_secs / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded generator, csrc/datagen.cpp; stands in for GIST1M)",
-            "config": {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96,
-                       "T1": 4, "T2": 15, "parallelism": "replicas" if world > 1 else "1gpu",
-                       "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},
-            "build_seconds": max_secs / args.steps,
-            "wall_seconds_timed": wall,
-            "pair_checks_per_build": stats[-1].edits.pair_checks,
-            "stage_seconds": {"scan": st0.scan_seconds, "sort": st0.sort_seconds,
-                              "apply": st0.apply_seconds, "reverse": st0.reverse_seconds},
-            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "traffic_algorithmic_bytes_same_launch": traffic_alg,
-                         "traffic_source": traffic_src,
-                         "kernel": "k_scan (distance stage)",
-                         "algorithmic_bytes_per_build": alg_bytes,
-                         "touched": st0.touched, "active_entries": st0.active_entries,
-                         "peak_source": peak_src},
-            "cpu_baseline": cpu,
-            "e2e": e2e,
-            "gpu_launches": launches,
-            "clocks": clk.summary(),
-            "recall": recall,
-        }
-        print(json.dumps(line))
-    if world > 1:
-        torch.distributed.destroy_process_group()
+    line = {
+        "metric": METRIC, "value": value, "unit": "dist-evals/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * max_secs / args.steps, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded generator, csrc/datagen.cpp; stands in for GIST1M)",
+        "config": {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96,
+                   "T1": 4, "T2": 15, "parallelism": "1gpu",
+                   "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},
+        "build_seconds": max_secs / args.steps,
+        "wall_seconds_timed": wall,
+        "pair_checks_per_build": stats[-1].edits.pair_checks,
+        "stage_seconds": {"scan": st0.scan_seconds, "sort": st0.sort_seconds,
+                          "apply": st0.apply_seconds, "reverse": st0.reverse_seconds},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "traffic": traffic,
+                     "traffic_algorithmic_bytes_same_launch": traffic_alg,
+                     "traffic_source": traffic_src,
+                     "kernel": "k_scan (distance stage)",
+                     "algorithmic_bytes_per_build": alg_bytes,
+                     "touched": st0.touched, "active_entries": st0.active_entries,
+                     "peak_source": peak_src},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clk.summary(),
+        "recall": recall,
+    }
+    print(json.dumps(line))
 
 
 if __name__ == "__main__":

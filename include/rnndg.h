@@ -176,6 +176,11 @@ int rnndg_set_partition(rnndg_ctx* ctx, uint64_t v_begin, uint64_t v_end);
 /* mark + scan of the owned lists; `partial` gets removed / flag_skips /
  * pair_checks of this shard; the redirects are staged as records */
 int rnndg_shard_scan(rnndg_ctx* ctx, rnndg_counts* partial, uint64_t* nrecords);
+/* totals of this shard's scans since the last reset: distance-stage seconds
+ * (CUDA events), touched entries T and active entries A, pass
+ * count.  No reference counterpart (measurement only). */
+int rnndg_shard_totals(rnndg_ctx* ctx, double* scan_seconds, uint64_t* touched,
+                       uint64_t* active_entries, uint64_t* passes, int reset);
 /* stage reverse proposals or in-edges of the owned lists */
 int rnndg_shard_stage(rnndg_ctx* ctx, int kind, uint64_t* nrecords);
 /* staged records sorted by dst into DEVICE buffers (nrecords each) and the

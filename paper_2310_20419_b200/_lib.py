@@ -83,6 +83,7 @@ def lib() -> C.CDLL:
         "rnndg_set_partition": (C.c_int, [vp, C.c_uint64, C.c_uint64]),
         "rnndg_shard_scan": (C.c_int, [vp, C.POINTER(Counts), u64p]),
         "rnndg_shard_stage": (C.c_int, [vp, C.c_int, u64p]),
+        "rnndg_shard_totals": (C.c_int, [vp, C.POINTER(C.c_double), u64p, u64p, u64p, C.c_int]),
         "rnndg_shard_export": (C.c_int, [vp, u64p, C.c_uint32, vp, vp, u64p]),
         "rnndg_shard_import": (C.c_int, [vp, C.c_int, vp, vp, C.c_uint64, C.c_uint32,
                                          C.POINTER(Counts), u64p]),
@@ -111,5 +112,5 @@ EXPORTED = (
     "rnndg_index_bytes", "rnndg_degree_stats", "rnndg_search", "rnndg_brute_force",
     "rnndg_rng_strategy", "rnndg_l2_pairs", "rnndg_synth_dim", "rnndg_synth",
     "rnndg_set_partition", "rnndg_shard_scan", "rnndg_shard_stage", "rnndg_shard_export",
-    "rnndg_shard_import", "rnndg_shard_out_prune",
+    "rnndg_shard_import", "rnndg_shard_out_prune", "rnndg_shard_totals",
 )

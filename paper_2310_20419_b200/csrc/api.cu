@@ -451,9 +451,23 @@ int rnndg_shard_scan(rnndg_ctx* c, rnndg_counts* partial, uint64_t* nrecords) {
     need_graph(c);
     if (!c->has_distances) throw ParamError("update_neighbors: graph has no distances");
     rnndg_counts cc{};
-    const uint64_t m = op_shard_scan(c, &cc, nullptr, nullptr);
+    const uint64_t m = op_shard_scan(c, &cc);
     if (partial) *partial = cc;
     if (nrecords) *nrecords = m;
+  });
+}
+
+int rnndg_shard_totals(rnndg_ctx* c, double* scan_seconds, uint64_t* touched,
+                       uint64_t* active_entries, uint64_t* passes, int reset) {
+  return guarded(c, [&] {
+    if (scan_seconds) *scan_seconds = c->shard_scan_s;
+    if (touched) *touched = c->shard_touched;
+    if (active_entries) *active_entries = c->shard_active;
+    if (passes) *passes = c->shard_passes;
+    if (reset) {
+      c->shard_scan_s = 0.0;
+      c->shard_touched = c->shard_active = c->shard_passes = 0;
+    }
   });
 }
 

@@ -940,15 +940,16 @@ void ensure_records(rnndg_ctx* c, uint64_t cap) {
 }
 
 // one pass's scan on the owned lists; redirects staged as records
-uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial, uint64_t* touched,
-                       uint64_t* active_entries) {
+uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial) {
   op_scan_phase(c);
   ensure_records(c, c->span);
   if (c->span)
     RNNDG_LAUNCH(c, k_pend_records, grid_for(c->span, 256, 148 * 64), 256, 0, c->span,
                  c->pend_src.p, c->pend_key.p, c->rec_cursor.p, c->rec_dst.p, c->rec_key.p);
   // counters of the scan phase (removed, flag_skips, pair_checks)
-  op_read_counters(c, partial, nullptr, nullptr, nullptr, touched, active_entries);
+  op_read_counters(c, partial, &c->shard_scan_s, nullptr, nullptr, &c->shard_touched,
+                   &c->shard_active);
+  ++c->shard_passes;
   return records_staged(c);
 }
 

@@ -140,6 +140,10 @@ struct rnndg_ctx {
   std::vector<rnndg_counts> pass_counts;
   bool trace = false;  // RNNDG_TRACE=1: per-pass line on stderr
   bool scan_cfg_logged = false;
+  // shard scans since the last rnndg_shard_totals(reset): distance-stage time
+  // and the SURVEY 8(d) units, for the sharded bench roofline
+  double shard_scan_s = 0.0;
+  uint64_t shard_touched = 0, shard_active = 0, shard_passes = 0;
   // timing events
   cudaEvent_t ev[8] = {};
 };
@@ -166,8 +170,7 @@ void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t
 void op_reverse(rnndg_ctx* c, uint32_t R, int order);
 void op_sort_lists(rnndg_ctx* c);
 void op_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end);
-uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial, uint64_t* touched,
-                       uint64_t* active_entries);
+uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial);
 uint64_t op_shard_stage(rnndg_ctx* c, int kind);
 void op_shard_export(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint32_t* dst_dev,
                      uint64_t* key_dev, uint64_t* counts);

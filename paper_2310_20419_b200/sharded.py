@@ -110,16 +110,34 @@ class DeviceShard:
     """One rank's share on a GPU: an rnndg context owning [v_begin, v_end)."""
 
     def __init__(self, data: np.ndarray, v_begin: int, v_end: int, device: int = 0):
-        from .rnnd import Device, VectorStore
+        from .rnnd import Device
         import torch
         self.torch = torch
         self.device = device
         self.dev = Device(device)
+        self.v_begin, self.v_end = v_begin, v_end
+        self.load(data)
+        self._nstaged = 0
+
+    def load(self, data: np.ndarray):
+        """(Re)upload the whole store from host memory (H2D) and own
+        [v_begin, v_end) again."""
+        from .rnnd import VectorStore
         self.store = VectorStore(data)
         self.dev.set_data(self.store)
-        self.dev.check(self.dev._L.rnndg_set_partition(self.dev.h, v_begin, v_end))
-        self.v_begin, self.v_end = v_begin, v_end
-        self._nstaged = 0
+        self.dev.check(self.dev._L.rnndg_set_partition(self.dev.h, self.v_begin, self.v_end))
+
+    def launches(self) -> int:
+        return self.dev.launches()
+
+    def totals(self, reset: bool = False) -> dict:
+        """Distance-stage seconds and SURVEY 8(d) units of this shard's scans."""
+        s = C.c_double()
+        t, a, p = C.c_uint64(), C.c_uint64(), C.c_uint64()
+        self._check(self.dev._L.rnndg_shard_totals(self.dev.h, C.byref(s), C.byref(t), C.byref(a),
+                                                   C.byref(p), int(reset)))
+        return {"scan_seconds": s.value, "touched": t.value, "active_entries": a.value,
+                "passes": p.value}
 
     def _check(self, rc):
         self.dev.check(rc)

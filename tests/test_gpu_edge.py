@@ -1,0 +1,142 @@
+"""GPU parity on the build's edge cases: whole builds through the C ABI against
+the oracle (itself pinned to rnnd::build), bit-exact per-pass EditCounts and
+index bytes.
+
+Cases the reference's own tests touch (builder.cpp:253-289 parameter range,
+test_builder.cpp:255-297) plus the data shapes that stress the device
+formulation: exact duplicates (zero distances, id tie-breaks), rows shorter
+than one 32-float block (tail-only chains), one block plus a tail, overflow
+to +inf distances, subnormal / zero distances, S = n - 1, R = 1, T1 = 1, and
+both prune orders.  A full-size (BASELINE C3, 1M x 960) build is checked
+through size-independent properties.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def R():
+    from paper_2310_20419_b200 import rnnd
+    return rnnd
+
+
+def counts_of(c):
+    return [int(c.removed), int(c.inserted), int(c.flag_skips), int(c.pair_checks)]
+
+
+def check_build(R, oracle, data, S, Rr, T1, T2, seed=42, order=0):
+    data = np.ascontiguousarray(data, np.float32)
+    st = R.BuildStats()
+    g = R.build(R.VectorStore(data),
+                R.BuildParams(S=S, R=Rr, T1=T1, T2=T2, seed=seed,
+                              prune_order=R.PruneOrder(order)), st)
+    og = oracle.OracleGraph(data)
+    rc, pc = og.build(S=S, R=Rr, T1=T1, T2=T2, seed=seed, order=order)
+    assert rc == 0
+    assert [counts_of(c) for c in st.pass_counts] == pc.tolist()
+    assert R.index_bytes(g) == og.index_bytes()
+    return g
+
+
+def rng(seed):
+    return np.random.default_rng(seed)
+
+
+def test_exact_duplicates(R, oracle):
+    base = rng(1).random((12, 6), dtype=np.float32)
+    data = np.repeat(base, 20, axis=0)  # 240 rows, 20 copies of each point
+    rng(2).shuffle(data)
+    check_build(R, oracle, data, S=10, Rr=12, T1=3, T2=3)
+
+
+def test_all_points_identical(R, oracle):
+    data = np.full((64, 5), 0.25, np.float32)
+    check_build(R, oracle, data, S=8, Rr=10, T1=2, T2=2)
+
+
+@pytest.mark.parametrize("d", [1, 2, 3, 5, 31, 32, 33, 63, 65])
+def test_short_rows(R, oracle, d):
+    """d < 32: tail-only chains; d = 33 / 65: block(s) plus a one-element tail."""
+    data = oracle.synth_uniform(300, d, 7 + d)
+    check_build(R, oracle, data, S=8, Rr=12, T1=2, T2=3)
+
+
+def test_one_dimension_many_ties(R, oracle):
+    data = (rng(3).integers(0, 16, (400, 1))).astype(np.float32)  # heavy distance ties
+    check_build(R, oracle, data, S=10, Rr=10, T1=3, T2=3)
+
+
+def test_overflow_to_inf(R, oracle):
+    """Squared differences near FLT_MAX: many distances round to +inf, which
+    must order and occlude exactly as in the reference (inf >= inf)."""
+    data = (rng(4).random((200, 8)) * 3e19).astype(np.float32)
+    check_build(R, oracle, data, S=8, Rr=10, T1=2, T2=3)
+
+
+def test_subnormal_and_zero_distances(R, oracle):
+    data = (rng(5).random((200, 12)) * 1e-22).astype(np.float32)
+    check_build(R, oracle, data, S=8, Rr=10, T1=2, T2=3)
+
+
+@pytest.mark.parametrize("n,S", [(2, 1), (3, 2), (5, 4), (33, 32)])
+def test_tiny_stores_s_is_n_minus_1(R, oracle, n, S):
+    data = oracle.synth_uniform(n, 4, n)
+    check_build(R, oracle, data, S=S, Rr=S, T1=3, T2=2)
+
+
+@pytest.mark.parametrize("Rr,T1,T2,order", [(1, 3, 2, 0), (1, 3, 2, 1), (5, 1, 1, 0),
+                                             (5, 1, 6, 0), (200, 3, 2, 1), (8, 6, 1, 1)])
+def test_parameter_extremes(R, oracle, Rr, T1, T2, order):
+    data = oracle.synth_uniform(250, 10, 21)
+    check_build(R, oracle, data, S=12, Rr=Rr, T1=T1, T2=T2, order=order)
+
+
+def test_seed_changes_graph_deterministically(R, oracle):
+    data = oracle.synth_uniform(300, 8, 5)
+    a = check_build(R, oracle, data, S=10, Rr=12, T1=2, T2=2, seed=1)
+    b = check_build(R, oracle, data, S=10, Rr=12, T1=2, T2=2, seed=2)
+    assert R.index_bytes(a) != R.index_bytes(b)
+
+
+@pytest.mark.slow
+def test_full_size_properties(R, oracle):
+    """BASELINE C3 at full size (1M x 960): too large for the oracle, so the
+    graph is checked through properties that hold at any size: lists sorted
+    nearest-first with unique ids and no self loops, every cached distance
+    equal to the exact reference l2 of its endpoints (a sample of 20k
+    entries, bit-exact), per-pass counter identities (inserted <= removed),
+    and determinism (a second build gives identical bytes)."""
+    from paper_2310_20419_b200 import datagen
+    cfg = datagen.CONFIGS["C3-gistlike-1M"]
+    data = datagen.rows(cfg.cfg, cfg.seed, 0, cfg.n)
+    store = R.VectorStore(data)
+    dev = R.Device()
+    dev.set_data(store)
+    st = R.BuildStats()
+    g = R.build(store, R.BuildParams(), st, device=dev)
+    c = g.csr
+    off = c.offsets.astype(np.int64)
+    ids = c.ids.astype(np.int64)
+    dists = c.dists
+    n = len(off) - 1
+    assert n == cfg.n
+    lens = np.diff(off)
+    assert lens.min() >= 1
+    src = np.repeat(np.arange(n), lens)
+    assert not np.any(ids == src)
+    # sorted by (dist, id) within each list, hence ids unique per list
+    same = src[1:] == src[:-1]
+    d0, d1 = dists[:-1][same], dists[1:][same]
+    i0, i1 = ids[:-1][same], ids[1:][same]
+    assert np.all((d0 < d1) | ((d0 == d1) & (i0 < i1)))
+    # cached distances == exact reference l2 (oracle, metric.hpp:26-65)
+    pick = np.random.default_rng(0).choice(len(ids), 20000, replace=False)
+    for j in pick[:20000]:
+        assert np.float32(dists[j]).view(np.uint32) == \
+            np.float32(oracle.l2_sq(data[src[j]], data[ids[j]])).view(np.uint32)
+    for pc in st.pass_counts:
+        assert pc.inserted <= pc.removed
+    g2 = R.build(store, R.BuildParams(), device=dev)
+    assert R.index_bytes(g2) == R.index_bytes(g)
