@@ -24,9 +24,10 @@
 // lifetime, so fewer vertices are in flight and their rows stay in L2 between
 // push steps (ncu: a warp-per-vertex scan re-read rows from HBM at every step).
 //
-//   k_scan_block<2, false>   lists <= kScanUcap; keys + alive list in smem
-//   k_scan_block<32, true>   longer lists (hubs that collect redirects), on a
-//                            second stream concurrently
+//   k_scan_spec<2, false, 4>   lists <= kScanUcap; keys + alive list in smem
+//   k_scan_spec<32, true, 4>   longer lists (hubs that collect redirects), on
+//                              a second stream concurrently
+// (k_scan_block: the same walk with two steps per round; RNNDG_SPEC=0)
 #include <cstdio>
 #include <cstdlib>
 
@@ -41,6 +42,7 @@ namespace {
 constexpr int kShortWarps = 4;   // staged / sliced experiments: 128-thread CTAs
 constexpr int kPushWarps = 2;    // default push scan: one 64-thread CTA per short list
 constexpr int kLongWarps = 32;   // one 1024-thread CTA per long list
+constexpr int kSpec = 4;         // provisional kept entries per push round
 
 // Chain-blocked row layout: element e < d4 = d - d % 4 lives at
 //   32 * (e / 32) + 8 * (e % 4) + (e % 32) / 4
@@ -452,6 +454,227 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_block(ScanArgs g) {
       if (w2kept) {
         if (tid == 0) L[nk] = wk2 & ~1ull;
         ++nk;
+      }
+      na = nn;
+    }
+    if (tid == 0) g.post_cnt[u] = nk;
+    for (uint32_t j = tid; j < U; j += NT) touched += T[j];
+    __syncthreads();
+  }
+  flush_counters(g.ctr, removed, checks, skips, touched);
+}
+
+// ------------------------------------------------------------ speculative
+// Order-preserving block-wide exclusive scan of per-thread counts c.
+template <int W>
+__device__ __forceinline__ uint32_t block_excl_scan(uint32_t c, uint32_t* wcnt,
+                                                    uint32_t& total) {
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  uint32_t x = c;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= uint32_t(o)) x += y;
+  }
+  if (lane == 31) wcnt[wid] = x;
+  __syncthreads();
+  uint32_t before = 0, tot = 0;
+#pragma unroll
+  for (int w = 0; w < W; ++w) {
+    const uint32_t v = wcnt[w];
+    before += uint32_t(w) < wid ? v : 0u;
+    tot += v;
+  }
+  total = tot;
+  __syncthreads();
+  return before + x - c;
+}
+
+// k_scan_block with D push steps per round.  The first D alive candidates
+// w_1..w_D are provisionally kept and every later candidate is evaluated
+// against all of them in the same round (one task per needed pair).  The
+// fates of w_2..w_D are then resolved in list order (w_j is kept iff no kept
+// w_i, i < j, occludes it), and each candidate walks w_1..w_D in order,
+// counting only pairs with kept entries and stopping at its first occluder --
+// the reference's exact sequence of skips and checks (builder.cpp:50-64).
+// Pairs evaluated against a w_j that turns out occluded are not counted.
+template <int W, bool kLong, int D>
+__global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
+  constexpr uint32_t NT = 32 * W;
+  constexpr uint32_t kCap = kLong ? 1 : kScanUcap;
+  constexpr uint32_t kTasks = NT * D;
+  __shared__ uint64_t keys_sh[kCap];
+  __shared__ uint32_t alive_sh[kCap];
+  __shared__ uint32_t tq[kTasks];  // task: list position of the candidate
+  __shared__ uint8_t tw[kTasks];   //       which provisional entry (0 .. D-1)
+  __shared__ float tres[kTasks];   //       their distance
+  __shared__ uint32_t wcnt[W];
+  __shared__ uint32_t s_a, s_kept;
+  __shared__ uint32_t s_tb[D];     // task base of candidates 1 .. D-1
+  __shared__ uint32_t s_nm[D];     // their need masks
+  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  const uint32_t quad = lane >> 2, chain = lane & 3;
+  const Row row = g.row;
+  const uint32_t row_bytes = row.stride * 4u;
+  const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount]) : uint32_t(*g.nsmall);
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
+
+  for (;;) {
+    if (tid == 0) s_a = atomicAdd(g.work + (kLong ? 1 : 0), 1u);
+    __syncthreads();
+    const uint32_t a = s_a;
+    if (a >= nq) break;
+    const uint32_t u = kLong ? g.act_list[g.n + a] : uint32_t(g.act_small[a]);
+    const uint64_t base = g.off[u];
+    const uint32_t U = g.cnt[u];
+    uint64_t* L = g.keys + base;
+    uint8_t* T = g.touch + base;
+    const uint64_t* K = kLong ? L : keys_sh;
+    uint32_t* A = kLong ? g.alive_g + base : alive_sh;
+    for (uint32_t j = tid; j < U; j += NT) {
+      const uint64_t k = L[j];
+      if (!kLong) keys_sh[j] = k;
+      A[j] = j;
+      prefetch_row_l2(row(k), row_bytes);
+    }
+    __syncthreads();
+    uint32_t na = U, nk = 0;
+    while (na) {
+      const uint32_t De = na < uint32_t(D) ? na : uint32_t(D);
+      uint64_t wk[D];
+      uint32_t wp[D];
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        wp[i] = uint32_t(i) < De ? A[i] : A[0];
+        wk[i] = K[wp[i]];
+      }
+      __syncthreads();  // all threads have read A[0 .. De) / K[p]
+      uint32_t nn = 0;  // survivors so far, compacted in place into A[0 ..)
+      uint32_t kept = 1u;  // bit i: w_{i+1} kept (known after the first batch)
+      for (uint32_t b0 = 1; b0 < na; b0 += NT) {
+        const uint32_t ai = b0 + tid;
+        const bool valid = ai < na;
+        const uint32_t q = valid ? A[ai] : 0u;
+        const uint64_t vk = valid ? K[q] : 0ull;
+        const bool vf = key_fresh(vk);
+        // candidate ai is tested against w_1 .. w_min(D, ai)
+        const uint32_t lim = valid ? (ai < De ? ai : De) : 0u;
+        uint32_t nm = 0;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          if (uint32_t(i) < lim && (key_fresh(wk[i]) || vf)) nm |= 1u << i;
+        uint32_t ntask;
+        const uint32_t tb = block_excl_scan<W>(__popc(nm), wcnt, ntask);
+        {
+          uint32_t t = tb;
+#pragma unroll
+          for (int i = 0; i < D; ++i)
+            if (nm >> i & 1u) {
+              tq[t] = q;
+              tw[t] = uint8_t(i);
+              ++t;
+            }
+        }
+        if (ai < uint32_t(D)) {  // provisional entries (first batch only)
+          s_tb[ai] = tb;
+          s_nm[ai] = valid ? nm : 0u;
+        }
+        __syncthreads();
+        for (uint32_t t0 = 0; t0 < ntask; t0 += 8 * W) {
+          const uint32_t twp = t0 + 8 * wid;
+          if (twp >= ntask) continue;  // warp-uniform
+          const uint32_t ti = twp + quad;
+          const bool has = ti < ntask;
+          const uint32_t ts = has ? ti : twp;
+          const uint64_t vkey = K[tq[ts]];
+          const float* xv = row(vkey);
+          const uint32_t wsel = tw[ts];
+          uint64_t wkey = wk[0];
+#pragma unroll
+          for (int i = 1; i < D; ++i)
+            if (wsel == uint32_t(i)) wkey = wk[i];
+          const float dist = quad_l2(xv, row(wkey), chain, row.nblk, row.ntail);
+          if (has && chain == 0) tres[ti] = dist;
+        }
+        __syncthreads();
+        if (b0 == 1) {
+          // fates of w_2 .. w_De, in list order
+          if (tid == 0) {
+            uint32_t kb = 1u;
+            for (uint32_t j = 1; j < De; ++j) {
+              const float dj = key_dist(wk[j]);
+              uint32_t t = s_tb[j];
+              bool occl = false;
+              for (uint32_t i = 0; i < j; ++i) {
+                if (!(s_nm[j] >> i & 1u)) continue;
+                const float d = tres[t++];
+                if ((kb >> i & 1u) && dj >= d) {
+                  occl = true;
+                  break;
+                }
+              }
+              if (!occl) kb |= 1u << j;
+            }
+            s_kept = kb;
+          }
+          __syncthreads();
+          kept = s_kept;
+        }
+        // walk w_1 .. w_lim in order over the kept ones
+        bool gone = false;
+        uint32_t by = 0;
+        float dvw = 0.f;
+        {
+          uint32_t t = tb;
+#pragma unroll
+          for (int i = 0; i < D; ++i) {
+            if (uint32_t(i) >= lim || gone) continue;
+            const bool nd = nm >> i & 1u;
+            const float d = nd ? tres[t] : 0.f;
+            if (nd) ++t;
+            if (!(kept >> i & 1u)) continue;  // not in the reference's kept list
+            if (!nd) {
+              ++skips;
+              continue;
+            }
+            ++checks;
+            T[q] = 1;
+            T[wp[i]] = 1;
+            if (key_dist(vk) >= d) {
+              gone = true;
+              by = uint32_t(i);
+              dvw = d;
+            }
+          }
+        }
+        if (gone) {
+          ++removed;
+          uint64_t wkey = wk[0];
+#pragma unroll
+          for (int i = 1; i < D; ++i)
+            if (by == uint32_t(i)) wkey = wk[i];
+          const uint32_t w_id = key_id(wkey);
+          g.pend_src[base + q] = w_id;
+          g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
+          if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
+        }
+        // survivors stay alive; kept provisional entries leave the alive list
+        const bool stay = valid && !gone && !(ai < De && (kept >> ai & 1u));
+        uint32_t nstay;
+        const uint32_t r = block_rank<W>(stay, wcnt, nstay);
+        if (stay) A[nn + r] = q;
+        nn += nstay;
+        __syncthreads();
+      }
+      // kept entries, flagged old (builder.cpp:68), in list order
+      if (tid == 0) {
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          if (uint32_t(i) < De && (kept >> i & 1u)) L[nk++] = wk[i] & ~1ull;
+      } else {
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          if (uint32_t(i) < De && (kept >> i & 1u)) ++nk;
       }
       na = nn;
     }
@@ -1047,6 +1270,18 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
                : short_w == 2 ? k_scan_block<2, false, false>
                : short_w == 4 ? k_scan_block<4, false, false>
                               : k_scan_block<8, false, false>;
+  // provisional kept entries per push round: RNNDG_SPEC = 2 | 3 | 4 (default
+  // 4, k_scan_spec) or 0 (k_scan_block, two steps per round).  At C3 1M:
+  // 2 -> 2.89 s, 3 -> 2.78 s, 4 -> 2.77 s, 6 -> 3.37 s per build.
+  static const int spec = [] {
+    const char* e = std::getenv("RNNDG_SPEC");
+    const int v = e ? std::atoi(e) : kSpec;
+    return v == 0 || v == 2 || v == 3 ? v : kSpec;
+  }();
+  if (spec == 2) kpush = short_w == 4 ? k_scan_spec<4, false, 2> : k_scan_spec<2, false, 2>;
+  if (spec == 3) kpush = short_w == 4 ? k_scan_spec<4, false, 3> : k_scan_spec<2, false, 3>;
+  if (spec == kSpec) kpush = short_w == 4 ? k_scan_spec<4, false, kSpec>
+                                          : k_scan_spec<2, false, kSpec>;
   auto kshort = stage ? k_scan_block<kShortWarps, false, true>
                       : (sliced ? k_scan_sliced<kShortWarps>
                                 : (push ? kpush
@@ -1077,11 +1312,18 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
                  int(stage), int(sliced), a.nslots, smem, per_sm);
     c->scan_cfg_logged = true;
   }
+  if (const char* e = std::getenv("RNNDG_CTAS_PER_SM")) {  // tuning: cap resident CTAs
+    const int v = std::atoi(e);
+    if (v > 0 && v < per_sm) per_sm = v;
+  }
   const unsigned grid = unsigned(sm_count(c)) * unsigned(per_sm > 0 ? per_sm : 1);
   // fork: the side stream waits for everything issued so far on the main one
   RNNDG_CUDA(cudaEventRecord(c->ev_fork, c->stream));
   RNNDG_CUDA(cudaStreamWaitEvent(c->side, c->ev_fork, 0));
-  k_scan_block<kLongWarps, true, false><<<unsigned(sm_count(c)) / 4, 32 * kLongWarps, 0, c->side>>>(a);
+  if (spec == 0)
+    k_scan_block<kLongWarps, true, false><<<unsigned(sm_count(c)) / 4, 32 * kLongWarps, 0, c->side>>>(a);
+  else
+    k_scan_spec<kLongWarps, true, kSpec><<<unsigned(sm_count(c)) / 4, 32 * kLongWarps, 0, c->side>>>(a);
   ++c->launches;
   RNNDG_CUDA(cudaGetLastError());
   RNNDG_LAUNCH(c, kshort, grid, threads_short, smem, a);
