@@ -33,6 +33,7 @@
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "ctx.hpp"
@@ -134,7 +135,7 @@ __global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
                               uint8_t* __restrict__ active,
                               uint32_t* __restrict__ act_list,
                               uint32_t* __restrict__ post_cnt,
-                              unsigned long long* __restrict__ ctr) {
+                              unsigned long long* __restrict__ ctr, uint32_t ucap) {
   const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned long long skips = 0, aentries = 0, nact = 0;
   bool large = false;
@@ -151,7 +152,7 @@ __global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
     if (act) {
       aentries = U;
       nact = 1;
-      large = U > kScanUcap;
+      large = U > ucap;
       flag = large ? 2 : 1;
       atomicMax(&ctr[kMaxLen], (unsigned long long)U);
     } else {
@@ -202,6 +203,13 @@ __global__ void k_order_keys(uint64_t n, const uint32_t* __restrict__ label,
                              uint64_t* __restrict__ okey) {
   const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   if (u < n) okey[u] = (uint64_t(label[u]) << 32) | u;
+}
+
+// longest lists first (ties by index): the persistent scan's tail is short
+__global__ void k_len_keys(uint64_t n, const uint32_t* __restrict__ cnt,
+                           uint64_t* __restrict__ okey) {
+  const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (u < n) okey[u] = (uint64_t(0xFFFFFFFFu - cnt[u]) << 32) | u;
 }
 
 struct IsShortActive {
@@ -689,31 +697,60 @@ void merge_and_swap(rnndg_ctx* c, const uint32_t* post_cnt) {
 
 // Locality order of the short active lists into c->act_small; count into
 // work[2] (read by the scan kernel).
+// lists longer than this go to the 1024-thread hub kernel (RNNDG_UCAP,
+// at most kScanUcap, the short kernel's shared-memory capacity).  C3 1M:
+// 512 -> 2.51 s, 256 -> 2.46 s, 128 -> 2.56 s, 64 -> 3.25 s per build.
+uint32_t hub_threshold() {
+  static const uint32_t v = [] {
+    const char* e = std::getenv("RNNDG_UCAP");
+    const int x = e ? std::atoi(e) : 256;
+    return uint32_t(x >= 32 && x <= int(kScanUcap) ? x : 256);
+  }();
+  return v;
+}
+
 void locality_order(rnndg_ctx* c) {
   const uint64_t n = c->nv;
   if (n == 0) {
     zero(c, c->work.p + 2, 1);
     return;
   }
+  // RNNDG_ORDER: 0 = vertex index (default), 1 = locality labels (3 label
+  // rounds + radix sort; no faster scan at C3 1M once hubs use every SM, and
+  // 40 ms per build of its own), 2 = longest list first
+  static const int mode = [] {
+    const char* e = std::getenv("RNNDG_ORDER");
+    return e ? std::atoi(e) : 0;
+  }();
   uint32_t* la = c->label.p;
   uint32_t* lb = c->label.p + n;
-  // a shard's lists point at vertices it does not own: order by index there
-  RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
-               nullptr, la, int(c->partitioned));
-  for (int r = 1; r < kLabelRounds && !c->partitioned; ++r) {
-    RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
-                 la, lb, 0);
-    std::swap(la, lb);
-  }
   uint64_t* ok = c->okey.p;
   uint64_t* ok2 = c->okey.p + n;
-  RNNDG_LAUNCH(c, k_order_keys, grid_for(n, 256), 256, 0, n, la, ok);
   size_t bytes = 0;
-  RNNDG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, ok, ok2, int64_t(n), 0, 64,
-                                            c->stream));
-  RNNDG_CUDA(cub::DeviceRadixSort::SortKeys(cub_temp(c, bytes), bytes, ok, ok2, int64_t(n), 0,
-                                            64, c->stream));
-  c->launches += 8;
+  if (mode == 0) {
+    RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
+                 nullptr, la, 1);
+    RNNDG_LAUNCH(c, k_order_keys, grid_for(n, 256), 256, 0, n, la, ok2);  // already sorted
+  } else {
+    if (mode == 2) {
+      RNNDG_LAUNCH(c, k_len_keys, grid_for(n, 256), 256, 0, n, c->cnt.p, ok);
+    } else {
+      // a shard's lists point at vertices it does not own: order by index there
+      RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
+                   nullptr, la, int(c->partitioned));
+      for (int r = 1; r < kLabelRounds && !c->partitioned; ++r) {
+        RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p,
+                     c->key.p, la, lb, 0);
+        std::swap(la, lb);
+      }
+      RNNDG_LAUNCH(c, k_order_keys, grid_for(n, 256), 256, 0, n, la, ok);
+    }
+    RNNDG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, ok, ok2, int64_t(n), 0, 64,
+                                              c->stream));
+    RNNDG_CUDA(cub::DeviceRadixSort::SortKeys(cub_temp(c, bytes), bytes, ok, ok2, int64_t(n), 0,
+                                              64, c->stream));
+    c->launches += 8;
+  }
   int* nsel = reinterpret_cast<int*>(c->work.p + 2);
   bytes = 0;
   RNNDG_CUDA(cub::DeviceSelect::If(nullptr, bytes, ok2, c->act_small.p, nsel, int64_t(n),
@@ -772,7 +809,7 @@ void op_scan_phase(rnndg_ctx* c) {
   RNNDG_CUDA(cudaEventRecord(c->ev[0], c->stream));
   if (n)
     RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
-                 c->active.p, c->act_list.p, c->post_cnt.p, ctr);
+                 c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold());
   locality_order(c);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
   launch_scan(c, c->work.p);
