@@ -135,64 +135,6 @@ __device__ __forceinline__ float quad_l2(const float* __restrict__ a, const floa
   return sum;
 }
 
-// quad_l2 with D blocks of each operand in flight per lane (same chain
-// order: blocks are consumed strictly in sequence).
-template <int D>
-__device__ __forceinline__ float quad_l2_deep(const float* __restrict__ a,
-                                              const float* __restrict__ b, uint32_t k,
-                                              uint32_t nblk, uint32_t ntail) {
-  float s = 0.f;
-  const float* pa = a + 8 * k;
-  const float* pb = b + 8 * k;
-  float ra[D][8], rb[D][8];
-  uint32_t blk = 0;
-  if (nblk >= D) {
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      ld256(pa + 32 * i, ra[i]);
-      ld256(pb + 32 * i, rb[i]);
-    }
-    for (blk = D; blk + D <= nblk; blk += D) {
-#pragma unroll
-      for (int i = 0; i < D; ++i) {
-        chain_step(ra[i], rb[i], s);
-        ld256(pa + 32 * (blk + i), ra[i]);
-        ld256(pb + 32 * (blk + i), rb[i]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i) {
-      chain_step(ra[i], rb[i], s);
-      if (blk + i < nblk) {
-        ld256(pa + 32 * (blk + i), ra[i]);
-        ld256(pb + 32 * (blk + i), rb[i]);
-      }
-    }
-#pragma unroll
-    for (int i = 0; i < D; ++i)
-      if (blk + i < nblk) chain_step(ra[i], rb[i], s);
-  } else {
-    for (; blk < nblk; ++blk) {
-      ld256(pa + 32 * blk, ra[0]);
-      ld256(pb + 32 * blk, rb[0]);
-      chain_step(ra[0], rb[0], s);
-    }
-  }
-  const float s_next = __shfl_down_sync(0xffffffffu, s, 1);
-  const float pair = __fadd_rn(s, s_next);
-  const float pair2 = __shfl_down_sync(0xffffffffu, pair, 2);
-  float sum = __fadd_rn(pair, pair2);
-  if (ntail && k == 0) {
-    const float* ta = a + 32 * nblk;
-    const float* tb = b + 32 * nblk;
-    for (uint32_t t = 0; t < ntail; ++t) {
-      const float df = __fsub_rn(__ldg(ta + t), __ldg(tb + t));
-      sum = __fadd_rn(sum, __fmul_rn(df, df));
-    }
-  }
-  return sum;
-}
-
 // Same as quad_l2 on generic pointers (rows staged in shared memory or in
 // global memory): two 128-bit loads per block and operand.
 __device__ __forceinline__ float quad_l2_any(const float* a, const float* b, uint32_t k,
@@ -556,7 +498,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t c, uint32_t* wcnt,
 // counting only pairs with kept entries and stopping at its first occluder --
 // the reference's exact sequence of skips and checks (builder.cpp:50-64).
 // Pairs evaluated against a w_j that turns out occluded are not counted.
-template <int W, bool kLong, int D, int kDepth = 2>
+template <int W, bool kLong, int D>
 __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   constexpr uint32_t NT = 32 * W;
   constexpr uint32_t kCap = kLong ? 1 : kScanUcap;
@@ -651,9 +593,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
 #pragma unroll
           for (int i = 1; i < D; ++i)
             if (wsel == uint32_t(i)) wkey = wk[i];
-          const float dist =
-              kDepth == 2 ? quad_l2(xv, row(wkey), chain, row.nblk, row.ntail)
-                          : quad_l2_deep<kDepth>(xv, row(wkey), chain, row.nblk, row.ntail);
+          const float dist = quad_l2(xv, row(wkey), chain, row.nblk, row.ntail);
           if (has && chain == 0) tres[ti] = dist;
         }
         __syncthreads();
@@ -1342,12 +1282,6 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   if (spec == 3) kpush = short_w == 4 ? k_scan_spec<4, false, 3> : k_scan_spec<2, false, 3>;
   if (spec == kSpec) kpush = short_w == 4 ? k_scan_spec<4, false, kSpec>
                                           : k_scan_spec<2, false, kSpec>;
-  static const int depth = [] {
-    const char* e = std::getenv("RNNDG_DEPTH");
-    return e ? std::atoi(e) : 2;
-  }();
-  if (spec == kSpec && depth == 3) kpush = k_scan_spec<2, false, kSpec, 3>;
-  if (spec == kSpec && depth == 4) kpush = k_scan_spec<2, false, kSpec, 4>;
   auto kshort = stage ? k_scan_block<kShortWarps, false, true>
                       : (sliced ? k_scan_sliced<kShortWarps>
                                 : (push ? kpush
