@@ -60,25 +60,6 @@ uint32_t crc32_ieee(const uint8_t* p, size_t size) {
 }
 
 // device CSR (capacity layout) -> host (counts, keys) in list order
-void fetch_graph(rnndg_ctx* c, std::vector<uint64_t>& off, std::vector<uint32_t>& cnt,
-                 std::vector<uint64_t>& keys) {
-  const uint64_t n = c->nv;
-  off.resize(n + 1);
-  cnt.resize(n);
-  RNNDG_CUDA(cudaMemcpyAsync(off.data(), c->off.p, (n + 1) * 8, cudaMemcpyDeviceToHost, c->stream));
-  RNNDG_CUDA(cudaMemcpyAsync(cnt.data(), c->cnt.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
-  keys.resize(c->span ? c->span : 1);
-  if (c->span)
-    RNNDG_CUDA(cudaMemcpyAsync(keys.data(), c->key.p, c->span * 8, cudaMemcpyDeviceToHost, c->stream));
-  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
-}
-
-float bits_to_float(uint32_t b) {
-  float f;
-  std::memcpy(&f, &b, 4);
-  return f;
-}
-
 }  // namespace
 
 extern "C" {
@@ -274,12 +255,7 @@ int rnndg_pass_counts(const rnndg_ctx* c, rnndg_counts* out, uint32_t cap) {
 int rnndg_graph_size(rnndg_ctx* c, uint64_t* n, uint64_t* edges) {
   return guarded(c, [&] {
     need_graph(c);
-    std::vector<uint32_t> cnt(c->nv);
-    if (c->nv)
-      RNNDG_CUDA(cudaMemcpyAsync(cnt.data(), c->cnt.p, c->nv * 4, cudaMemcpyDeviceToHost, c->stream));
-    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
-    uint64_t m = 0;
-    for (uint32_t v : cnt) m += v;
+    const uint64_t m = op_export(c, nullptr, nullptr, nullptr, nullptr);
     if (n) *n = c->nv;
     if (edges) *edges = m;
   });
@@ -289,20 +265,7 @@ int rnndg_get_graph(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists
                     uint8_t* fresh) {
   return guarded(c, [&] {
     need_graph(c);
-    std::vector<uint64_t> off, keys;
-    std::vector<uint32_t> cnt;
-    fetch_graph(c, off, cnt, keys);
-    uint64_t w = 0;
-    for (uint64_t u = 0; u < c->nv; ++u) {
-      if (offsets) offsets[u] = w;
-      for (uint32_t j = 0; j < cnt[u]; ++j, ++w) {
-        const uint64_t k = keys[off[u] + j];
-        if (ids) ids[w] = key_id(k);
-        if (dists) dists[w] = bits_to_float(key_dbits(k));
-        if (fresh) fresh[w] = uint8_t(key_fresh(k));
-      }
-    }
-    if (offsets) offsets[c->nv] = w;
+    op_export(c, offsets, ids, dists, fresh);  // compacted on the device
   });
 }
 
@@ -359,14 +322,13 @@ int rnndg_set_graph(rnndg_ctx* c, uint64_t n, const uint64_t* offsets, const uin
 int rnndg_index_bytes(rnndg_ctx* c, uint8_t* buf, uint64_t* size) {
   return guarded(c, [&] {
     need_graph(c);
-    std::vector<uint64_t> off, keys;
-    std::vector<uint32_t> cnt;
-    fetch_graph(c, off, cnt, keys);
-    uint64_t m = 0;
-    for (uint32_t v : cnt) m += v;
+    const uint64_t m = op_export(c, nullptr, nullptr, nullptr, nullptr);
     const uint64_t total = 16 + (c->nv + 1) * 8 + m * 4 + 4;
     if (size) *size = total;
     if (!buf) return;
+    std::vector<uint64_t> offs(c->nv + 1);
+    std::vector<uint32_t> ids(m ? m : 1);
+    op_export(c, offs.data(), ids.data(), nullptr, nullptr);
     // graph.cpp:102-126: "RNND", u32 version 1, u64 n, u64 offsets[n+1],
     // u32 ids, u32 CRC-32 of everything before; little-endian
     uint8_t* p = buf;
@@ -381,14 +343,8 @@ int rnndg_index_bytes(rnndg_ctx* c, uint8_t* buf, uint64_t* size) {
     p += 4;
     put32(1);
     put64(c->nv);
-    uint64_t o = 0;
-    put64(o);
-    for (uint64_t u = 0; u < c->nv; ++u) {
-      o += cnt[u];
-      put64(o);
-    }
-    for (uint64_t u = 0; u < c->nv; ++u)
-      for (uint32_t j = 0; j < cnt[u]; ++j) put32(key_id(keys[off[u] + j]));
+    for (uint64_t u = 0; u <= c->nv; ++u) put64(offs[u]);
+    for (uint64_t j = 0; j < m; ++j) put32(ids[j]);
     put32(crc32_ieee(buf, size_t(p - buf)));
   });
 }

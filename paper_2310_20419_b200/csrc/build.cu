@@ -324,6 +324,27 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// Dense CSR for the host: entry j of list u goes to doff[u] + j, unpacked
+// into id / dist / fresh (graph.hpp NeighborEntry fields).
+__global__ void __launch_bounds__(kBlock)
+    k_export(uint64_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+             const uint64_t* __restrict__ key, const uint64_t* __restrict__ doff,
+             uint32_t* __restrict__ ids, float* __restrict__ dists,
+             uint8_t* __restrict__ fresh) {
+  const uint32_t lane = lane_id();
+  WARP_LOOP(u, n) {
+    const uint64_t* P = key + off[u];
+    const uint64_t w = doff[u];
+    const uint32_t U = cnt[u];
+    for (uint32_t j = lane; j < U; j += 32) {
+      const uint64_t k = P[j];
+      ids[w + j] = key_id(k);
+      dists[w + j] = __uint_as_float(uint32_t(k >> 32));
+      fresh[w + j] = uint8_t(k & 1u);
+    }
+  }
+}
+
 // Copy lists without tombstones (order, hence sortedness, is preserved).
 __global__ void __launch_bounds__(kBlock)
     k_compact(uint64_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ cnt,
@@ -855,6 +876,34 @@ void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t
                  h[kActiveCount], h[kLargeCount], h[kMaxLen], h[kActiveEntries], h[kPairChecks],
                  h[kRemoved], h[kInserted], h[kTouched], elapsed_ms(c->ev[0], c->ev[1]),
                  elapsed_ms(c->ev[1], c->ev[2]), elapsed_ms(c->ev[2], c->ev[3]));
+}
+
+uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,
+                   uint8_t* fresh) {
+  const uint64_t n = c->nv;
+  c->ex_off.ensure(n + 1);
+  scan_u32(c, c->cnt.p, c->ex_off.p, n);
+  uint64_t m = 0;
+  RNNDG_CUDA(cudaMemcpyAsync(&m, c->ex_off.p + n, 8, cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  if (m && (ids || dists || fresh)) {
+    c->ex_ids.ensure(m);
+    c->ex_dists.ensure(m);
+    c->ex_fresh.ensure(m);
+    RNNDG_LAUNCH(c, k_export, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
+                 c->ex_off.p, c->ex_ids.p, c->ex_dists.p, c->ex_fresh.p);
+    if (ids)
+      RNNDG_CUDA(cudaMemcpyAsync(ids, c->ex_ids.p, m * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (dists)
+      RNNDG_CUDA(cudaMemcpyAsync(dists, c->ex_dists.p, m * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (fresh)
+      RNNDG_CUDA(cudaMemcpyAsync(fresh, c->ex_fresh.p, m, cudaMemcpyDeviceToHost, c->stream));
+  }
+  if (offsets)
+    RNNDG_CUDA(cudaMemcpyAsync(offsets, c->ex_off.p, (n + 1) * 8, cudaMemcpyDeviceToHost,
+                               c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  return m;
 }
 
 void op_update_pass(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t_sort,

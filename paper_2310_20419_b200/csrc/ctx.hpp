@@ -119,6 +119,11 @@ struct rnndg_ctx {
   rnndg::DevBuf<uint32_t> post_cnt;
   rnndg::DevBuf<unsigned long long> counters;
   rnndg::DevBuf<unsigned int> work;
+  // dense CSR staging for rnndg_get_graph (device-side compaction)
+  rnndg::DevBuf<uint64_t> ex_off;
+  rnndg::DevBuf<uint32_t> ex_ids;
+  rnndg::DevBuf<float> ex_dists;
+  rnndg::DevBuf<uint8_t> ex_fresh;
   rnndg::DevBuf<uint32_t> kpos_g;  // scan scratch for lists > kScanUcap
   // sharding: staged (dst, key) records, per-part counts
   rnndg::DevBuf<uint32_t> rec_dst, rec_dst2;
@@ -171,6 +176,10 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order);
 void op_sort_lists(rnndg_ctx* c);
 void op_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end);
 uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial);
+// dense CSR (graph.hpp view) of the owned lists into host arrays (any may be
+// null); returns the edge count
+uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,
+                   uint8_t* fresh);
 uint64_t op_shard_stage(rnndg_ctx* c, int kind);
 void op_shard_export(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint32_t* dst_dev,
                      uint64_t* key_dev, uint64_t* counts);
