@@ -82,41 +82,30 @@ __device__ __forceinline__ uint32_t lower_bound(const uint64_t* a, uint32_t m, u
   for (uint64_t var = warp_; var < (count); var += nwarps_)
 
 // ------------------------------------------------------------- random init
-// graph.cpp:47-63.  One warp per vertex: lane 0 runs Floyd's sampling
-// (rng.hpp:46-72; the emitted-set test is a linear scan, which is exactly the
-// reference's S <= 64 branch and equivalent to its hash-set branch), then the
-// warp computes the S cached distances.
-template <bool kVec4>
+// graph.cpp:47-63.  One thread per vertex runs Floyd's sampling (rng.hpp:46-72;
+// the emitted-set test is a linear scan, which is exactly the reference's
+// S <= 64 branch and equivalent to its hash-set branch) and leaves the raw
+// samples in the keys; k_init_dists (scan.cu) shifts them past the pivot and
+// computes the S cached distances.
 __global__ void k_random_init(uint64_t n, uint64_t v0, uint64_t nv, uint32_t S, uint64_t seed,
-                              const float* __restrict__ x, uint32_t d,
                               uint64_t* __restrict__ key) {
-  const uint32_t lane = lane_id();
-  WARP_LOOP(ul, nv) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t ul = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; ul < nv; ul += stride) {
     const uint64_t u = v0 + ul;  // global id: the stream and the pivot are global
     uint64_t* out = key + ul * S;
-    if (lane == 0) {
-      SplitMix64 rng(mix_seed(seed, u));
-      const uint32_t domain = uint32_t(n - 1);  // exclude u
-      uint32_t m = 0;
-      for (uint32_t j = domain - S; j < domain; ++j) {
-        uint32_t t = uint32_t(rng.bounded(uint64_t(j) + 1));
-        bool hit = false;
-        for (uint32_t q = 0; q < m; ++q)
-          if (uint32_t(out[q]) == t) {
-            hit = true;
-            break;
-          }
-        out[m++] = hit ? j : t;
-      }
+    SplitMix64 rng(mix_seed(seed, u));
+    const uint32_t domain = uint32_t(n - 1);  // exclude u
+    uint32_t m = 0;
+    for (uint32_t j = domain - S; j < domain; ++j) {
+      uint32_t t = uint32_t(rng.bounded(uint64_t(j) + 1));
+      bool hit = false;
+      for (uint32_t q = 0; q < m; ++q)
+        if (uint32_t(out[q]) == t) {
+          hit = true;
+          break;
+        }
+      out[m++] = hit ? j : t;
     }
-    __syncwarp();
-    for (uint32_t j = lane; j < S; j += 32) {
-      uint32_t id = uint32_t(out[j]);
-      if (id >= u) ++id;  // shift past the excluded pivot (rng.hpp:68-70)
-      float dist = l2_exact<kVec4>(x + u * d, x + uint64_t(id) * d, d);
-      out[j] = make_key(dist, id, 1u);
-    }
-    __syncwarp();
   }
 }
 
@@ -585,7 +574,8 @@ __global__ void k_part_counts(uint64_t nr, const uint32_t* __restrict__ rdst,
 
 // ------------------------------------------------------------- host glue
 
-unsigned grid_for(uint64_t items, unsigned block, unsigned cap = 1u << 20) {
+// one thread per item unless `cap` is given (then the kernel must be grid-stride)
+unsigned grid_for(uint64_t items, unsigned block, unsigned cap = 0x7fffffffu) {
   uint64_t g = (items + block - 1) / block;
   if (g < 1) g = 1;
   if (g > cap) g = cap;
@@ -802,12 +792,11 @@ void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
   c->key.ensure(c->span ? c->span : 1);
   RNNDG_LAUNCH(c, k_fill_offsets, grid_for(nv + 1, 256), 256, 0, nv, S, c->off.p, c->cnt.p);
   if (nv) {
-    if (c->d % 4 == 0)
-      RNNDG_LAUNCH(c, k_random_init<true>, warp_grid(c, nv), kBlock, 0, n, c->v0, nv, S, seed,
-                   c->x, c->d, c->key.p);
-    else
-      RNNDG_LAUNCH(c, k_random_init<false>, warp_grid(c, nv), kBlock, 0, n, c->v0, nv, S, seed,
-                   c->x, c->d, c->key.p);
+    // ids here; the S cached distances per vertex with the scan's quad L2 on
+    // the chain-blocked rows (coalesced 128-byte lines per quad)
+    RNNDG_LAUNCH(c, k_random_init, grid_for(nv, 128), 128, 0, n, c->v0, nv, S, seed,
+                 c->key.p);
+    launch_init_dists(c, S);
   }
   c->has_graph = true;
   c->has_distances = true;

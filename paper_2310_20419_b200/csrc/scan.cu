@@ -1168,6 +1168,28 @@ __global__ void __launch_bounds__(32 * W) k_scan_pull(ScanArgs g) {
   flush_counters(g.ctr, removed, checks, skips, touched);
 }
 
+// Cached distances of the random initial lists (graph.cpp:53-61), a quad per
+// (u, id) pair on the chain-blocked rows.  key[p] holds the raw Floyd sample
+// of pair p = ul * S + j (not yet shifted past the pivot u, rng.hpp:68-70).
+__global__ void __launch_bounds__(256) k_init_dists(uint64_t nv, uint64_t v0, uint32_t S,
+                                                   Row row, uint64_t* __restrict__ key) {
+  const uint32_t lane = lane_id(), quad = lane >> 2, chain = lane & 3;
+  const uint64_t total = nv * S;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t p0 = warp * 8; p0 < total; p0 += nwarps * 8) {
+    const uint64_t p = p0 + quad;
+    const bool has = p < total;
+    const uint64_t ps = has ? p : p0;
+    const uint64_t u = v0 + ps / S;
+    uint32_t id = uint32_t(key[ps]);
+    if (id >= u) ++id;
+    const float dist = quad_l2(row.xp + u * row.stride, row.xp + uint64_t(id) * row.stride, chain,
+                               row.nblk, row.ntail);
+    if (has && chain == 0) key[ps] = make_key(dist, id, 1u);
+  }
+}
+
 }  // namespace
 
 ScanConfig scan_config(rnndg_ctx* c) {
@@ -1178,6 +1200,19 @@ ScanConfig scan_config(rnndg_ctx* c) {
   cfg.ntail = d - d4;
   cfg.stride = cfg.nblk * 32 + (cfg.ntail ? 8 : 0);
   return cfg;
+}
+
+void launch_init_dists(rnndg_ctx* c, uint32_t S) {
+  const ScanConfig cfg = scan_config(c);
+  prepare_chain_layout(c);
+  const uint64_t total = c->nv * S;
+  if (!total) return;
+  const Row row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail};
+  const uint64_t groups = (total + 7) / 8;  // 8 pairs per warp
+  uint64_t blocks = (groups + 7) / 8;       // 8 warps per block
+  const uint64_t cap = uint64_t(sm_count(c)) * 8;
+  if (blocks > cap) blocks = cap;
+  RNNDG_LAUNCH(c, k_init_dists, unsigned(blocks), 256, 0, c->nv, c->v0, S, row, c->key.p);
 }
 
 void prepare_chain_layout(rnndg_ctx* c) {

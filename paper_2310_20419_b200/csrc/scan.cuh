@@ -22,5 +22,8 @@ struct ScanConfig {
 ScanConfig scan_config(rnndg_ctx* c);
 void prepare_chain_layout(rnndg_ctx* c);
 void launch_scan(rnndg_ctx* c, unsigned int* work);
+// cached distances of the random initial lists (k_random_init left the raw
+// samples in the keys' low 32 bits)
+void launch_init_dists(rnndg_ctx* c, uint32_t S);
 
 }  // namespace rnndg
