@@ -107,6 +107,12 @@ int rnndg_set_data(rnndg_ctx* ctx, const float* rows, uint64_t n, uint32_t d);
 /* borrows rows already resident on the context's device */
 int rnndg_set_data_device(rnndg_ctx* ctx, const float* rows_dev, uint64_t n,
                           uint32_t d);
+/* replaces rnnd::load_fvecs (dataset.cpp:82-95) + rnndg_set_data: reads an
+ * .fvecs file in chunks through pinned staging buffers, validates it with the
+ * reference's checks and messages (parse_vecs, dataset.cpp:55-78; non-finite
+ * values, :89) and streams it to the device with async H2D copies.  Errors
+ * are RNNDG_EDATA with "<path>: <reason>". */
+int rnndg_load_fvecs(rnndg_ctx* ctx, const char* path, uint64_t* n, uint32_t* d);
 
 /* ---- hot path ---- */
 int rnndg_random_init(rnndg_ctx* ctx, uint32_t S, uint64_t seed);

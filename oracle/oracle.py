@@ -285,6 +285,8 @@ def ref_lib():
                                 C.c_uint32, C.c_uint64, C.c_int, C.c_int, f64p]
         L.ref_export.argtypes = [C.c_void_p, u64p, u32p, f32p, u8p]
         L.ref_import.argtypes = [C.c_void_p, u64p, u32p, f32p, u8p]
+        L.ref_load_vecs.restype = C.c_int
+        L.ref_load_vecs.argtypes = [C.c_char_p, C.c_int, u64p, u64p, C.c_char_p, C.c_uint64]
         L.ref_index_bytes.restype = C.c_uint64
         L.ref_index_bytes.argtypes = [C.c_void_p, u8p, C.c_uint64]
         L.ref_batch_search.restype = C.c_double
@@ -373,3 +375,17 @@ def ref_brute_force(base, queries, k, threads=0):
                               _p(queries, f32p), queries.shape[0], k, threads,
                               _p(ids, u32p))
     return ids
+
+
+def ref_load_vecs(path: str, ivecs: bool = False):
+    """The reference's own load_fvecs / load_ivecs: (n, d) or the DataError
+    message (str)."""
+    n = np.zeros(1, np.uint64)
+    d = np.zeros(1, np.uint64)
+    err = C.create_string_buffer(512)
+    rc = ref_lib().ref_load_vecs(os.fsencode(path), int(ivecs), _p(n, u64p), _p(d, u64p), err, 512)
+    if rc == 0:
+        return int(n[0]), int(d[0])
+    if rc == 2:
+        return err.value.decode()
+    raise RuntimeError("reference loader failed")

@@ -207,4 +207,27 @@ int ref_brute_force(const float* base, uint64_t n, uint32_t d,
   }
 }
 
+// load_fvecs / load_ivecs (dataset.cpp:82-119): 0 and (n, d) on success,
+// 2 (DataError) with the message copied into err, 3 otherwise
+int ref_load_vecs(const char* path, int ivecs, uint64_t* n, uint64_t* d, char* err,
+                  uint64_t err_cap) {
+  try {
+    if (ivecs) {
+      GroundTruth gt = load_ivecs(path);
+      *n = gt.rows();
+      *d = gt.k;
+    } else {
+      VectorStore st = load_fvecs(path);
+      *n = st.n;
+      *d = st.d;
+    }
+    return 0;
+  } catch (const DataError& e) {
+    std::snprintf(err, err_cap, "%s", e.what());
+    return 2;
+  } catch (...) {
+    return 3;
+  }
+}
+
 }  // extern "C"

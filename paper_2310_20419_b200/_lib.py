@@ -60,6 +60,7 @@ def lib() -> C.CDLL:
         "rnndg_kernel_launches": (C.c_uint64, [vp]),
         "rnndg_set_data": (C.c_int, [vp, f32p, C.c_uint64, C.c_uint32]),
         "rnndg_set_data_device": (C.c_int, [vp, vp, C.c_uint64, C.c_uint32]),
+        "rnndg_load_fvecs": (C.c_int, [vp, C.c_char_p, u64p, C.POINTER(C.c_uint32)]),
         "rnndg_random_init": (C.c_int, [vp, C.c_uint32, C.c_uint64]),
         "rnndg_update_pass": (C.c_int, [vp, C.POINTER(Counts)]),
         "rnndg_reverse": (C.c_int, [vp, C.c_uint32, C.c_int]),
@@ -106,7 +107,7 @@ def ptr(a, t):
 # every symbol include/rnndg.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "rnndg_create", "rnndg_destroy", "rnndg_last_error", "rnndg_kernel_launches",
-    "rnndg_set_data", "rnndg_set_data_device", "rnndg_random_init",
+    "rnndg_set_data", "rnndg_set_data_device", "rnndg_load_fvecs", "rnndg_random_init",
     "rnndg_update_pass", "rnndg_reverse", "rnndg_sort_lists", "rnndg_build",
     "rnndg_pass_counts", "rnndg_graph_size", "rnndg_get_graph", "rnndg_set_graph",
     "rnndg_index_bytes", "rnndg_degree_stats", "rnndg_search", "rnndg_brute_force",

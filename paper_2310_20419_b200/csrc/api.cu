@@ -129,6 +129,13 @@ int rnndg_set_data(rnndg_ctx* c, const float* rows, uint64_t n, uint32_t d) {
   });
 }
 
+int rnndg_load_fvecs(rnndg_ctx* c, const char* path, uint64_t* n, uint32_t* d) {
+  return guarded(c, [&] {
+    if (!path) throw ParamError("load_fvecs: path required");
+    op_load_fvecs(c, path, n, d);
+  });
+}
+
 int rnndg_set_data_device(rnndg_ctx* c, const float* rows_dev, uint64_t n, uint32_t d) {
   return guarded(c, [&] {
     if (!rows_dev || n == 0 || d == 0) throw ParamError("set_data: empty store");

@@ -176,6 +176,7 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order);
 void op_sort_lists(rnndg_ctx* c);
 void op_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end);
 uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial);
+void op_load_fvecs(rnndg_ctx* c, const char* path, uint64_t* n, uint32_t* d);
 // dense CSR (graph.hpp view) of the owned lists into host arrays (any may be
 // null); returns the edge count
 uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,

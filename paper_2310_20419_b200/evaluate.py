@@ -33,10 +33,13 @@ def _read(path: str) -> bytes:
         raise R.DataError(f"{path}: cannot open") from e
 
 
-def _parse_vecs(path: str, buf: bytes) -> Tuple[int, int, np.ndarray]:
-    """Record walk shared by both formats (dataset.cpp:55-78): each record is
-    a little-endian int32 dimension followed by that many 4-byte payloads;
-    every record must have the same positive dimension."""
+def _parse_vecs(path: str, buf: bytes, bad_value, value_msg: str) -> Tuple[int, int, np.ndarray]:
+    """Record walk shared by both formats (parse_vecs, dataset.cpp:55-78):
+    each record is a little-endian int32 dimension followed by that many
+    4-byte payloads; every record must have the same positive dimension.  As
+    in the reference, records are checked in file order -- a record's header,
+    then its values (`bad_value(words) -> bool mask`, `value_msg`), then the
+    next record -- and the first problem is reported."""
     if not buf:
         raise R.DataError(f"{path}: empty file")
     if len(buf) < 4:
@@ -48,9 +51,16 @@ def _parse_vecs(path: str, buf: bytes) -> Tuple[int, int, np.ndarray]:
     nrec = len(buf) // rec
     words = np.frombuffer(buf[:nrec * rec], "<u4").reshape(nrec, dim + 1) if nrec else \
         np.zeros((0, dim + 1), "<u4")
-    if np.any(words[:, 0].view("<i4") <= 0):
-        raise R.DataError(f"{path}: non-positive record dimension")
-    if np.any(words[:, 0] != dim):
+    hdr = words[:, 0].view("<i4")
+    bad_hdr = np.flatnonzero(hdr != dim)
+    first_hdr = int(bad_hdr[0]) if bad_hdr.size else nrec
+    bad_val = np.flatnonzero(np.any(bad_value(words[:, 1:]), axis=1))
+    first_val = int(bad_val[0]) if bad_val.size else nrec
+    if first_val < first_hdr:
+        raise R.DataError(f"{path}: {value_msg}")
+    if first_hdr < nrec:
+        if hdr[first_hdr] <= 0:
+            raise R.DataError(f"{path}: non-positive record dimension")
         raise R.DataError(f"{path}: record dimension mismatch")
     rest = len(buf) - nrec * rec
     if rest:
@@ -67,10 +77,9 @@ def _parse_vecs(path: str, buf: bytes) -> Tuple[int, int, np.ndarray]:
 
 def load_fvecs(path: str) -> R.VectorStore:
     """dataset.cpp:82-95: rejects NaN / Inf."""
-    nrec, dim, words = _parse_vecs(path, _read(path))
+    nrec, dim, words = _parse_vecs(
+        path, _read(path), lambda w: ~np.isfinite(w.view("<f4")), "non-finite value")
     data = np.ascontiguousarray(words).view("<f4").astype(np.float32)
-    if not np.all(np.isfinite(data)):
-        raise R.DataError(f"{path}: non-finite value")
     return R.VectorStore(data.reshape(nrec, dim))
 
 
@@ -84,9 +93,8 @@ def write_fvecs(store: R.VectorStore, path: str) -> None:
 
 
 def load_ivecs(path: str) -> R.GroundTruth:
-    nrec, dim, words = _parse_vecs(path, _read(path))
-    if np.any(words.view("<i4") < 0):
-        raise R.DataError(f"{path}: negative id")
+    """dataset.cpp:109-119: rejects negative ids."""
+    nrec, dim, words = _parse_vecs(path, _read(path), lambda w: w.view("<i4") < 0, "negative id")
     return R.GroundTruth(dim, np.ascontiguousarray(words).astype(np.uint32))
 
 

@@ -27,9 +27,10 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import os
 import time
 from dataclasses import dataclass, field
-from typing import Callable, List, Optional, Sequence
+from typing import Callable, List, Optional, Sequence, Tuple
 
 import numpy as np
 
@@ -124,6 +125,15 @@ def nearer(a: NeighborEntry, b: NeighborEntry) -> bool:
 
 # --------------------------------------------------------------- device
 
+@dataclass
+class DeviceStore:
+    """A VectorStore resident only on one context's device (Device.load_fvecs)."""
+
+    n: int
+    d: int
+    device: "Device"
+
+
 class Device:
     """One rnndg_ctx: a CUDA stream, device buffers, the store and a graph."""
 
@@ -158,6 +168,18 @@ class Device:
     def set_data(self, store: VectorStore):
         self.check(self._L.rnndg_set_data(self.h, ptr(store.data, f32p), store.n, store.d))
         self.store_ref = store
+
+    def load_fvecs(self, path: str) -> "DeviceStore":
+        """rnnd::load_fvecs (dataset.cpp:82-95) straight into this context's
+        device store: pinned staging, chunked, async H2D (rnndg_load_fvecs).
+        The store lives only on the device; pass the returned DeviceStore to
+        build() / batch_search() in place of a VectorStore."""
+        n = C.c_uint64()
+        d = C.c_uint32()
+        self.check(self._L.rnndg_load_fvecs(self.h, os.fsencode(path), C.byref(n), C.byref(d)))
+        ds = DeviceStore(int(n.value), int(d.value), self)
+        self.store_ref = ds
+        return ds
 
     def set_graph(self, csr: "CSR", has_distances: bool):
         n = len(csr.offsets) - 1
@@ -375,6 +397,8 @@ def build(store: VectorStore, params: BuildParams = BuildParams(),
           progress: Optional[BuildProgressFn] = None,
           device: Optional[Device] = None) -> AdjacencyGraph:
     """builder.cpp:253-289; returns the graph by value (device-resident)."""
+    if isinstance(store, DeviceStore):
+        device = store.device
     dev = device or Device()
     if dev.store_ref is not store:
         dev.set_data(store)
