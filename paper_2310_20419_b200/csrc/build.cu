@@ -706,8 +706,6 @@ void merge_and_swap(rnndg_ctx* c, const uint32_t* post_cnt) {
   c->span = total;
 }
 
-// Locality order of the short active lists into c->act_small; count into
-// work[2] (read by the scan kernel).
 // lists longer than this go to the 1024-thread hub kernel (RNNDG_UCAP,
 // at most kScanUcap, the short kernel's shared-memory capacity).  C3 1M:
 // 512 -> 2.51 s, 256 -> 2.46 s, 128 -> 2.56 s, 64 -> 3.25 s per build.
@@ -720,6 +718,8 @@ uint32_t hub_threshold() {
   return v;
 }
 
+// Order of the short active lists into c->act_small (RNNDG_ORDER, default
+// vertex index); count into work[2] (read by the scan kernel).
 void locality_order(rnndg_ctx* c) {
   const uint64_t n = c->nv;
   if (n == 0) {

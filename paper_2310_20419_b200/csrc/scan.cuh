@@ -8,8 +8,9 @@ struct rnndg_ctx;
 
 namespace rnndg {
 
-// lists up to this length keep their alive list in shared memory; longer ones
-// use global scratch at the list's CSR offset (and are scheduled first)
+// capacity of the short-list kernel's shared-memory key / alive arrays (the
+// hub threshold, build.cu hub_threshold(), is at most this); longer lists use
+// global scratch at the list's CSR offset
 constexpr uint32_t kScanUcap = 512;
 
 // chain-blocked device copy of the store (see k_chain_layout in scan.cu)
