@@ -101,6 +101,28 @@ const char* rnndg_last_error(const rnndg_ctx* ctx);
 /* number of this library's kernels launched on the context so far */
 uint64_t rnndg_kernel_launches(const rnndg_ctx* ctx);
 
+/* ---- NN-Descent baseline (nndescent.hpp:12-52) ----
+ * Canonical deferred join (see oracle/rnnd_oracle.c ro_nnd_pass): every pool
+ * is snapshotted, all pairs joined, and each pool becomes the `cap` nearest
+ * distinct entries of pool + proposals.  The reference's parallel join is
+ * order-dependent (per-vertex locks); this form is deterministic.
+ * Parameters and errors as NnDescentParams / NnDescent::NnDescent
+ * (nndescent.cpp:11-22); cap = max(pool ? pool : 2K, K). */
+int rnndg_nnd_init(rnndg_ctx* ctx, uint32_t K, uint32_t sample, uint32_t iters,
+                   uint32_t pool, uint64_t seed);            /* NnDescent + init() */
+int rnndg_nnd_pass(rnndg_ctx* ctx, uint64_t* new_entries);  /* join_pass() */
+/* pools, dense n x stride: cnt[n], ids / dists / fresh [n * stride] (any
+ * may be null); *cap_out = stride = max(cap, min(sample, n - 1)) -- init
+ * fills min(sample, n-1) entries even above the cap, and such a pool keeps
+ * its size (insert_candidate pops one entry per insertion) */
+int rnndg_nnd_pools(rnndg_ctx* ctx, uint32_t* cap_out, uint32_t* cnt, uint32_t* ids,
+                    float* dists, uint8_t* fresh);
+int rnndg_nnd_finalize(rnndg_ctx* ctx);                       /* finalize() -> graph */
+/* build_nndescent (nndescent.cpp:101-119): init, iters passes, finalize;
+ * stats->seconds (CUDA events), update_passes = iters */
+int rnndg_nnd_build(rnndg_ctx* ctx, uint32_t K, uint32_t sample, uint32_t iters,
+                    uint32_t pool, uint64_t seed, rnndg_build_stats* stats);
+
 /* ---- data (VectorStore, vector_store.hpp:12-20) ---- */
 /* copies n x d row-major fp32 host rows to the device (H2D) */
 int rnndg_set_data(rnndg_ctx* ctx, const float* rows, uint64_t n, uint32_t d);

@@ -185,6 +185,21 @@ class OracleGraph:
         lib().ro_graph_import(self.h, _p(off, u64p), _p(ids, u32p), _p(dists, f32p),
                               _p(fresh, u8p))
 
+    # -- NN-Descent baseline (canonical deferred join; rnnd_oracle.c)
+    def nnd_init(self, K, sample, iters=10, pool=0, seed=42) -> int:
+        _nnd_sigs(lib())
+        return lib().ro_nnd_init(self.h, self._dp(), self.d, K, sample, iters, pool, seed)
+
+    def nnd_pass(self, sample, cap) -> int:
+        _nnd_sigs(lib())
+        return int(lib().ro_nnd_pass(self.h, self._dp(), self.d, sample, cap))
+
+    def nnd_finalize(self, K) -> "OracleGraph":
+        _nnd_sigs(lib())
+        out = OracleGraph(self.data)
+        lib().ro_nnd_finalize(self.h, K, out.h)
+        return out
+
     def index_bytes(self) -> bytes:
         size = lib().ro_index_bytes(self.h, None)
         buf = np.zeros(size, np.uint8)
@@ -216,6 +231,19 @@ def l2_sq(a, b) -> float:
     a = np.ascontiguousarray(a, np.float32)
     b = np.ascontiguousarray(b, np.float32)
     return float(np.float32(lib().ro_l2_sq(_p(a, f32p), _p(b, f32p), a.size)))
+
+
+def _nnd_sigs(L):
+    if getattr(L, "_nnd_sigs", False):
+        return
+    L.ro_nnd_init.restype = C.c_int
+    L.ro_nnd_init.argtypes = [C.c_void_p, f32p, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                              C.c_uint32, C.c_uint64]
+    L.ro_nnd_pass.restype = C.c_uint64
+    L.ro_nnd_pass.argtypes = [C.c_void_p, f32p, C.c_uint32, C.c_uint32, C.c_uint32]
+    L.ro_nnd_finalize.restype = None
+    L.ro_nnd_finalize.argtypes = [C.c_void_p, C.c_uint32, C.c_void_p]
+    L._nnd_sigs = True
 
 
 def synth_uniform(n, d, seed) -> np.ndarray:
@@ -389,3 +417,30 @@ def ref_load_vecs(path: str, ivecs: bool = False):
     if rc == 2:
         return err.value.decode()
     raise RuntimeError("reference loader failed")
+
+
+def ref_nndescent(data, K, sample, iters, pool=0, seed=42):
+    """The reference's own NnDescent with threads = 1: (pools after init as
+    (cnt, ids, dists) dense n x cap, final graph CSR)."""
+    data = np.ascontiguousarray(data, np.float32)
+    n, d = data.shape
+    # export stride: init fills min(sample, n-1) entries even above the cap
+    cap = max(pool if pool else 2 * K, K, min(sample, n - 1))
+    L = ref_lib()
+    L.ref_nndescent.restype = C.c_int
+    L.ref_nndescent.argtypes = [f32p, C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32,
+                                C.c_uint32, C.c_uint32, C.c_uint64, C.c_uint32, u32p, u32p,
+                                f32p, u64p, u32p, f32p]
+    pc = np.zeros(n, np.uint32)
+    pid = np.zeros(n * cap, np.uint32)
+    pd = np.zeros(n * cap, np.float32)
+    off = np.zeros(n + 1, np.uint64)
+    ids = np.zeros(n * K, np.uint32)
+    ds = np.zeros(n * K, np.float32)
+    rc = L.ref_nndescent(_p(data, f32p), n, d, K, sample, iters, pool, seed, cap, _p(pc, u32p),
+                         _p(pid, u32p), _p(pd, f32p), _p(off, u64p), _p(ids, u32p), _p(ds, f32p))
+    if rc:
+        return rc
+    m = int(off[n])
+    return (pc, pid.reshape(n, cap), pd.reshape(n, cap)), CSR(off, ids[:m], ds[:m],
+                                                               np.zeros(m, np.uint8))

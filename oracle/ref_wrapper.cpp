@@ -17,6 +17,7 @@
 
 #include "rnnd/builder.hpp"
 #include "rnnd/graph.hpp"
+#include "rnnd/nndescent.hpp"
 #include "rnnd/search.hpp"
 #include "rnnd/vector_store.hpp"
 
@@ -202,6 +203,52 @@ int ref_brute_force(const float* base, uint64_t n, uint32_t d,
     GroundTruth gt = brute_force_gt(b, q, k, threads);
     std::memcpy(ids, gt.ids.data(), sizeof(uint32_t) * gt.ids.size());
     return 0;
+  } catch (...) {
+    return 3;
+  }
+}
+
+// NnDescent (nndescent.cpp) with threads = 1 (deterministic): the pools after
+// init (pool_* arrays, dense n x cap, counts in pool_cnt) and the graph after
+// `iters` join passes + finalize (CSR).  1 on ParamError.
+int ref_nndescent(const float* data, uint64_t n, uint32_t d, uint32_t K, uint32_t sample,
+                  uint32_t iters, uint32_t pool, uint64_t seed, uint32_t cap,
+                  uint32_t* pool_cnt, uint32_t* pool_ids, float* pool_dists,
+                  uint64_t* offsets, uint32_t* ids, float* dists) {
+  try {
+    VectorStore st = make_store(data, n, d);
+    NnDescentParams p;
+    p.K = K;
+    p.sample = sample;
+    p.iters = iters;
+    p.pool = pool;
+    p.seed = seed;
+    p.threads = 1;
+    NnDescent nnd(st, p);
+    nnd.init();
+    for (uint64_t u = 0; u < n; ++u) {
+      const auto& pl = nnd.pools()[u];
+      pool_cnt[u] = uint32_t(pl.size());
+      for (size_t j = 0; j < pl.size() && j < cap; ++j) {
+        pool_ids[u * cap + j] = pl[j].id;
+        pool_dists[u * cap + j] = pl[j].dist;
+      }
+    }
+    for (uint32_t it = 0; it < iters; ++it) nnd.join_pass();
+    AdjacencyGraph g = nnd.finalize();
+    uint64_t w = 0;
+    for (uint64_t u = 0; u < n; ++u) {
+      offsets[u] = w;
+      for (const auto& e : g.adj[u]) {
+        ids[w] = e.id;
+        dists[w] = e.dist;
+        ++w;
+      }
+    }
+    offsets[n] = w;
+    return 0;
+  } catch (const ParamError&) {
+    return 1;
   } catch (...) {
     return 3;
   }

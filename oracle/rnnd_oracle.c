@@ -704,3 +704,150 @@ uint64_t ro_index_bytes(const ro_graph* g, uint8_t* b) {
   put_u32(b, &at, crc);
   return at;
 }
+
+/* ---------------------------------------------------- NN-Descent baseline */
+
+/* NnDescent::NnDescent + init, nndescent.cpp:11-37: pools start with
+ * s = min(sample, n-1) distinct random ids (the random_init sampler,
+ * stream mix_seed(seed, u)), fresh, sorted by nearer. */
+int ro_nnd_init(ro_graph* P, const float* data, uint32_t d, uint32_t K,
+                uint32_t sample, uint32_t iters, uint32_t pool, uint64_t seed) {
+  const uint64_t n = P->n;
+  if (n < 2) return 1;
+  if (K < 1 || K > n - 1) return 1;
+  if (sample < 1 || iters < 1) return 1;
+  (void)pool;
+  const uint32_t s = sample < n - 1 ? sample : (uint32_t)(n - 1);
+  if (ro_random_init(P, data, d, s, seed)) return 1;
+  ro_graph_sort_lists(P);
+  return 0;
+}
+
+typedef struct {
+  uint32_t dst, id;
+  float dist;
+} nnd_prop_t;
+
+static int cmp_entry_flag(const void* x, const void* y) {
+  /* nearer, then existing (old) entries before proposals of the same id */
+  const entry_t *a = (const entry_t*)x, *b = (const entry_t*)y;
+  if (nearer(a, b)) return -1;
+  if (nearer(b, a)) return 1;
+  return (int)a->fresh - (int)b->fresh;
+}
+
+static int cmp_prop_dst(const void* x, const void* y) {
+  const nnd_prop_t *a = (const nnd_prop_t*)x, *b = (const nnd_prop_t*)y;
+  return a->dst < b->dst ? -1 : a->dst > b->dst;
+}
+
+/* One join pass, canonical deferred form of NnDescent::join_pass
+ * (nndescent.cpp:51-86).  Snapshot every vertex first (its nearest `sample`
+ * fresh entries turn old and join; entries old before the pass join as old,
+ * :60-70); then every pair (fresh x fresh, fresh x old, :77-80) proposes each
+ * endpoint to the other's pool with d = l2_sq (:72-76); then each pool
+ * becomes the max(cap, its size) nearest distinct entries of (pool +
+ * proposals), new ones
+ * fresh, existing ones keeping their flags (insert_candidate's cap, dedupe
+ * and order, :39-49).  The reference applies proposals immediately under
+ * per-vertex locks, which is order-dependent for threads > 1; this form is
+ * order-free (l2_sq is bit-symmetric, so an id has one key per pool).
+ * Returns the number of entries in the new pools that were not in the old. */
+uint64_t ro_nnd_pass(ro_graph* P, const float* data, uint32_t d, uint32_t sample,
+                     uint32_t cap) {
+  const uint64_t n = P->n;
+  uint32_t* F = (uint32_t*)malloc(sizeof(uint32_t) * (size_t)n * sample);
+  uint32_t* fc = (uint32_t*)calloc(n, sizeof(uint32_t));
+  list_t* O = (list_t*)calloc(n, sizeof(list_t));
+  for (uint64_t u = 0; u < n; ++u) {
+    list_t* l = &P->adj[u];
+    for (uint32_t j = 0; j < l->size; ++j) {
+      entry_t* e = &l->e[j];
+      if (e->fresh && fc[u] < sample) {
+        F[u * sample + fc[u]++] = e->id;
+        e->fresh = 0;
+      } else if (!e->fresh) {
+        list_push(&O[u], *e);
+      }
+    }
+  }
+  nnd_prop_t* pr = NULL;
+  size_t np = 0, pcap = 0;
+#define NND_PUSH(a, b, dd)                                              \
+  do {                                                                  \
+    if (np + 2 > pcap) {                                                \
+      pcap = pcap ? 2 * pcap : 1024;                                    \
+      pr = (nnd_prop_t*)realloc(pr, sizeof(nnd_prop_t) * pcap);         \
+    }                                                                   \
+    pr[np].dst = (a); pr[np].id = (b); pr[np].dist = (dd); ++np;        \
+    pr[np].dst = (b); pr[np].id = (a); pr[np].dist = (dd); ++np;        \
+  } while (0)
+  for (uint64_t u = 0; u < n; ++u) {
+    const uint32_t* f = F + u * sample;
+    for (uint32_t i = 0; i < fc[u]; ++i)
+      for (uint32_t j = i + 1; j < fc[u]; ++j) {
+        const float dd = ro_l2_sq(data + (uint64_t)f[i] * d, data + (uint64_t)f[j] * d, d);
+        NND_PUSH(f[i], f[j], dd);
+      }
+    for (uint32_t i = 0; i < fc[u]; ++i)
+      for (uint32_t j = 0; j < O[u].size; ++j) {
+        const uint32_t o = O[u].e[j].id;
+        const float dd = ro_l2_sq(data + (uint64_t)f[i] * d, data + (uint64_t)o * d, d);
+        NND_PUSH(f[i], o, dd);
+      }
+  }
+#undef NND_PUSH
+  if (np) qsort(pr, np, sizeof(nnd_prop_t), cmp_prop_dst);
+  uint64_t inserted = 0;
+  size_t k = 0;
+  list_t tmp = {NULL, 0, 0};
+  for (uint64_t v = 0; v < n; ++v) {
+    list_t* l = &P->adj[v];
+    tmp.size = 0;
+    for (uint32_t j = 0; j < l->size; ++j) list_push(&tmp, l->e[j]);
+    const uint32_t old_n = l->size;
+    /* a pool larger than cap (init fills min(sample, n-1) entries) keeps its
+     * size: insert_candidate pops one entry per insertion (:46-47) */
+    const uint32_t lim = old_n > cap ? old_n : cap;
+    for (; k < np && pr[k].dst == v; ++k) {
+      entry_t x = {pr[k].id, pr[k].dist, 1};
+      list_push(&tmp, x);
+    }
+    if (tmp.size > 1) qsort(tmp.e, tmp.size, sizeof(entry_t), cmp_entry_flag);
+    /* dedupe by id (equal ids are adjacent: same dist) and cap */
+    entry_t* old = (entry_t*)malloc(sizeof(entry_t) * (old_n ? old_n : 1));
+    memcpy(old, l->e, sizeof(entry_t) * old_n);
+    l->size = 0;
+    for (uint32_t j = 0; j < tmp.size && l->size < lim; ++j) {
+      if (l->size && l->e[l->size - 1].id == tmp.e[j].id) continue;
+      list_push(l, tmp.e[j]);
+      int was = 0;
+      for (uint32_t q = 0; q < old_n; ++q)
+        if (old[q].id == tmp.e[j].id) { was = 1; break; }
+      inserted += !was;
+    }
+    free(old);
+  }
+  free(tmp.e);
+  free(pr);
+  for (uint64_t u = 0; u < n; ++u) free(O[u].e);
+  free(O);
+  free(fc);
+  free(F);
+  return inserted;
+}
+
+/* NnDescent::finalize, nndescent.cpp:88-99: the K nearest pool entries,
+ * flagged old. */
+void ro_nnd_finalize(const ro_graph* P, uint32_t K, ro_graph* out) {
+  for (uint64_t u = 0; u < P->n; ++u) {
+    const list_t* l = &P->adj[u];
+    list_t* o = &out->adj[u];
+    o->size = 0;
+    for (uint32_t j = 0; j < l->size && j < K; ++j) {
+      entry_t x = l->e[j];
+      x.fresh = 0;
+      list_push(o, x);
+    }
+  }
+}

@@ -89,6 +89,17 @@ void ro_degree_stats(const ro_graph* g, uint32_t cap, int has_distances,
 /* serialised index (graph.cpp:102-126); returns byte size, writes if buf */
 uint64_t ro_index_bytes(const ro_graph* g, uint8_t* buf);
 
+/* NN-Descent baseline (nndescent.cpp), canonical deferred join.  Pools are
+ * held as the lists of an ro_graph.  init validates like the constructor
+ * (nndescent.cpp:11-22; returns 1 on a parameter error) and fills the pools
+ * (:24-37); pass runs one deferred join (see rnnd_oracle.c) and returns the
+ * number of new pool entries; finalize keeps the K nearest (:88-99). */
+int ro_nnd_init(ro_graph* pools, const float* data, uint32_t d, uint32_t K,
+                uint32_t sample, uint32_t iters, uint32_t pool, uint64_t seed);
+uint64_t ro_nnd_pass(ro_graph* pools, const float* data, uint32_t d, uint32_t sample,
+                     uint32_t cap);
+void ro_nnd_finalize(const ro_graph* pools, uint32_t K, ro_graph* out);
+
 #ifdef __cplusplus
 }
 #endif

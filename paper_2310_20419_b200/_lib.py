@@ -89,6 +89,13 @@ def lib() -> C.CDLL:
         "rnndg_shard_import": (C.c_int, [vp, C.c_int, vp, vp, C.c_uint64, C.c_uint32,
                                          C.POINTER(Counts), u64p]),
         "rnndg_shard_out_prune": (C.c_int, [vp, C.c_uint32]),
+        "rnndg_nnd_init": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                     C.c_uint64]),
+        "rnndg_nnd_pass": (C.c_int, [vp, u64p]),
+        "rnndg_nnd_pools": (C.c_int, [vp, u32p, u32p, u32p, f32p, u8p]),
+        "rnndg_nnd_finalize": (C.c_int, [vp]),
+        "rnndg_nnd_build": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                      C.c_uint64, C.POINTER(BuildStatsC)]),
         "rnndg_synth_dim": (C.c_uint32, [C.c_int]),
         "rnndg_synth": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, f32p]),
     }
@@ -114,4 +121,6 @@ EXPORTED = (
     "rnndg_rng_strategy", "rnndg_l2_pairs", "rnndg_synth_dim", "rnndg_synth",
     "rnndg_set_partition", "rnndg_shard_scan", "rnndg_shard_stage", "rnndg_shard_export",
     "rnndg_shard_import", "rnndg_shard_out_prune", "rnndg_shard_totals",
+    "rnndg_nnd_init", "rnndg_nnd_pass", "rnndg_nnd_pools", "rnndg_nnd_finalize",
+    "rnndg_nnd_build",
 )

@@ -129,6 +129,86 @@ int rnndg_set_data(rnndg_ctx* c, const float* rows, uint64_t n, uint32_t d) {
   });
 }
 
+int rnndg_nnd_init(rnndg_ctx* c, uint32_t K, uint32_t sample, uint32_t iters, uint32_t pool,
+                   uint64_t seed) {
+  return guarded(c, [&] {
+    need_data(c);
+    op_nnd_init(c, K, sample, iters, pool, seed);
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int rnndg_nnd_pass(rnndg_ctx* c, uint64_t* new_entries) {
+  return guarded(c, [&] {
+    need_data(c);
+    const uint64_t m = op_nnd_pass(c);
+    if (new_entries) *new_entries = m;
+  });
+}
+
+int rnndg_nnd_pools(rnndg_ctx* c, uint32_t* cap_out, uint32_t* cnt, uint32_t* ids, float* dists,
+                    uint8_t* fresh) {
+  return guarded(c, [&] {
+    need_data(c);
+    if (!c->nd_ready) throw ParamError("nndescent: call init first");
+    const uint64_t n = c->n, cap = c->nd_stride;
+    if (cap_out) *cap_out = c->nd_stride;
+    if (cnt)
+      RNNDG_CUDA(cudaMemcpyAsync(cnt, c->nd_pcnt.p, n * 4, cudaMemcpyDeviceToHost, c->stream));
+    if (ids || dists || fresh) {
+      std::vector<uint64_t> keys(n * cap);
+      RNNDG_CUDA(cudaMemcpyAsync(keys.data(), c->nd_pool.p, n * cap * 8, cudaMemcpyDeviceToHost,
+                                 c->stream));
+      RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+      for (uint64_t i = 0; i < n * cap; ++i) {
+        const uint64_t k = keys[i];
+        if (ids) ids[i] = key_id(k);
+        if (dists) {
+          const uint32_t b = key_dbits(k);
+          std::memcpy(&dists[i], &b, 4);
+        }
+        if (fresh) fresh[i] = uint8_t(key_fresh(k));
+      }
+    }
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  });
+}
+
+int rnndg_nnd_finalize(rnndg_ctx* c) {
+  return guarded(c, [&] {
+    need_data(c);
+    op_nnd_finalize(c);
+  });
+}
+
+int rnndg_nnd_build(rnndg_ctx* c, uint32_t K, uint32_t sample, uint32_t iters, uint32_t pool,
+                    uint64_t seed, rnndg_build_stats* stats) {
+  return guarded(c, [&] {
+    need_data(c);
+    c->xp_src = nullptr;  // the chain-blocked copy is rebuilt inside the timed build
+    cudaEvent_t e0, e1;
+    RNNDG_CUDA(cudaEventCreate(&e0));
+    RNNDG_CUDA(cudaEventCreate(&e1));
+    RNNDG_CUDA(cudaEventRecord(e0, c->stream));
+    const uint64_t l0 = c->launches;
+    op_nnd_init(c, K, sample, iters, pool, seed);
+    for (uint32_t it = 0; it < iters; ++it) op_nnd_pass(c);
+    op_nnd_finalize(c);
+    RNNDG_CUDA(cudaEventRecord(e1, c->stream));
+    RNNDG_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    RNNDG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    if (stats) {
+      *stats = rnndg_build_stats{};
+      stats->seconds = ms * 1e-3;
+      stats->update_passes = iters;
+      stats->kernel_launches = c->launches - l0;
+    }
+  });
+}
+
 int rnndg_load_fvecs(rnndg_ctx* c, const char* path, uint64_t* n, uint32_t* d) {
   return guarded(c, [&] {
     if (!path) throw ParamError("load_fvecs: path required");

@@ -32,6 +32,7 @@
 #include <cub/device/device_select.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 
@@ -570,7 +571,6 @@ __global__ void k_part_counts(uint64_t nr, const uint32_t* __restrict__ rdst,
   counts[p] = lb(bounds[p + 1]) - lb(bounds[p]);
 }
 
-#undef WARP_LOOP
 
 // ------------------------------------------------------------- host glue
 
@@ -1144,5 +1144,294 @@ uint64_t op_shard_import(rnndg_ctx* c, int kind, const uint32_t* dst_dev, const 
 void op_shard_out_prune(rnndg_ctx* c, uint32_t R) {
   if (c->nv) RNNDG_LAUNCH(c, k_out_trunc, grid_for(c->nv, 256), 256, 0, c->nv, c->cnt.p, R);
 }
+
+// ------------------------------------------------------ NN-Descent baseline
+// nndescent.cpp, in the canonical deferred form the oracle restates
+// (oracle/rnnd_oracle.c ro_nnd_pass): per pass, snapshot every pool, join
+// every pair of the snapshot lists (launch_nnd_join), then make each pool the
+// `cap` nearest distinct entries of (pool + proposals) -- a segmented sort of
+// the union per vertex, deduplicated by id (an id has one key per pool: l2
+// is bit-symmetric) and truncated.  Proposals are produced and applied in
+// vertex chunks to bound memory; applying the union chunk by chunk gives the
+// same pools as applying it at once.
+namespace {
+
+constexpr uint64_t kNndChunkPairs = uint64_t(24) << 20;  // pairs per join chunk
+
+// random_init lists (stride S, sorted) -> pools (stride cap)
+__global__ void __launch_bounds__(kBlock)
+    k_nd_from_lists(uint64_t n, uint32_t cap, const uint64_t* __restrict__ off,
+                    const uint32_t* __restrict__ cnt, const uint64_t* __restrict__ key,
+                    uint64_t* __restrict__ pool, uint32_t* __restrict__ pcnt) {
+  const uint32_t lane = lane_id();
+  WARP_LOOP(u, n) {
+    const uint32_t U = cnt[u];
+    for (uint32_t j = lane; j < U; j += 32) pool[u * cap + j] = key[off[u] + j];
+    if (lane == 0) pcnt[u] = U;
+  }
+}
+
+// nndescent.cpp:60-70: the nearest `sample` fresh entries join as fresh and
+// turn old; entries old before the pass join as old.  Keeps a copy of the
+// pool (the new-entry count) and the pair count of the vertex.
+__global__ void k_nd_snapshot(uint64_t n, uint32_t cap, uint32_t sample,
+                              uint64_t* __restrict__ pool, const uint32_t* __restrict__ pcnt,
+                              uint32_t* __restrict__ F, uint32_t* __restrict__ fcnt,
+                              uint32_t* __restrict__ O, uint32_t* __restrict__ ocnt,
+                              uint64_t* __restrict__ pool0, uint32_t* __restrict__ pcnt0,
+                              uint32_t* __restrict__ npairs) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n; u += stride) {
+    uint64_t* P = pool + u * cap;
+    const uint32_t m = pcnt[u];
+    uint32_t fc = 0, oc = 0;
+    for (uint32_t j = 0; j < m; ++j) {
+      const uint64_t k = P[j];
+      if (key_fresh(k) && fc < sample) {
+        F[u * sample + fc++] = key_id(k);
+        P[j] = k & ~1ull;
+      } else if (!key_fresh(k)) {
+        O[u * cap + oc++] = key_id(k);
+      }
+      pool0[u * cap + j] = k;
+    }
+    fcnt[u] = fc;
+    ocnt[u] = oc;
+    pcnt0[u] = m;
+    npairs[u] = fc * (fc ? fc - 1 : 0) / 2 + fc * oc;
+  }
+}
+
+__global__ void k_nd_count_dst(uint64_t m, const uint32_t* __restrict__ dst,
+                               unsigned long long* __restrict__ cnt) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride)
+    atomicAdd(&cnt[dst[i]], 1ull);
+}
+
+// segment v = pool v (first) + its proposals; lengths into len (n + 1 slots)
+__global__ void k_nd_seg_len(uint64_t n, const uint32_t* __restrict__ pcnt,
+                             const unsigned long long* __restrict__ bcnt,
+                             unsigned long long* __restrict__ len) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t v = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; v < n; v += stride)
+    len[v] = pcnt[v] + bcnt[v];
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_nd_seg_fill(uint64_t n, uint32_t cap, const uint64_t* __restrict__ pool,
+                  const uint32_t* __restrict__ pcnt, const uint64_t* __restrict__ boff,
+                  uint64_t* __restrict__ seg, unsigned long long* __restrict__ cur) {
+  const uint32_t lane = lane_id();
+  WARP_LOOP(v, n) {
+    const uint32_t m = pcnt[v];
+    for (uint32_t j = lane; j < m; j += 32) seg[boff[v] + j] = pool[v * cap + j];
+    if (lane == 0) cur[v] = m;
+  }
+}
+
+__global__ void k_nd_scatter(uint64_t m, const uint32_t* __restrict__ dst,
+                             const uint64_t* __restrict__ key, const uint64_t* __restrict__ boff,
+                             unsigned long long* __restrict__ cur, uint64_t* __restrict__ seg) {
+  const uint64_t stride = uint64_t(gridDim.x) * blockDim.x;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < m; i += stride) {
+    const uint32_t v = dst[i];
+    seg[boff[v] + atomicAdd(&cur[v], 1ull)] = key[i];
+  }
+}
+
+// sorted union -> pool: drop repeated ids (the existing entry's even key
+// sorts before a proposal's odd one), keep the first cap (insert_candidate,
+// nndescent.cpp:39-49)
+__global__ void __launch_bounds__(kBlock)
+    k_nd_merge(uint64_t n, uint32_t cap_ref, uint32_t stride, const uint64_t* __restrict__ boff,
+               const uint64_t* __restrict__ seg, const uint32_t* __restrict__ pcnt0,
+               uint64_t* __restrict__ pool, uint32_t* __restrict__ pcnt) {
+  const uint32_t lane = lane_id();
+  WARP_LOOP(v, n) {
+    const uint64_t* S = seg + boff[v];
+    const uint32_t len = uint32_t(boff[v + 1] - boff[v]);
+    uint64_t* P = pool + v * stride;
+    // a pool above the cap (init fills min(sample, n-1)) keeps its size:
+    // insert_candidate pops one entry per insertion (nndescent.cpp:46-47)
+    const uint32_t cap = pcnt0[v] > cap_ref ? pcnt0[v] : cap_ref;
+    uint32_t w = 0;
+    uint64_t prev = ~0ull;  // previous element's key (id compare via >> 1)
+    for (uint32_t j0 = 0; j0 < len && w < cap; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      const uint64_t k = j < len ? S[j] : ~0ull;
+      uint64_t before = __shfl_up_sync(0xffffffffu, k, 1);
+      if (lane == 0) before = prev;
+      const bool keep = j < len && (k >> 1) != (before >> 1);
+      const unsigned mk = __ballot_sync(0xffffffffu, keep);
+      const uint32_t r = w + __popc(mk & ((1u << lane) - 1u));
+      if (keep && r < cap) P[r] = k;
+      w += __popc(mk);
+      prev = __shfl_sync(0xffffffffu, k, 31);
+    }
+    if (lane == 0) pcnt[v] = w < cap ? w : cap;
+  }
+}
+
+// entries of the new pool whose id was not in the pool before the pass
+__global__ void __launch_bounds__(kBlock)
+    k_nd_count_new(uint64_t n, uint32_t cap, const uint64_t* __restrict__ pool,
+                   const uint32_t* __restrict__ pcnt, const uint64_t* __restrict__ pool0,
+                   const uint32_t* __restrict__ pcnt0, unsigned long long* __restrict__ ctr) {
+  const uint32_t lane = lane_id();
+  unsigned long long fresh = 0;
+  WARP_LOOP(v, n) {
+    const uint64_t* P0 = pool0 + v * cap;
+    const uint32_t m0 = pcnt0[v];
+    for (uint32_t j = lane; j < pcnt[v]; j += 32) {
+      const uint64_t k = pool[v * cap + j] & ~1ull;
+      const uint32_t at = lower_bound(P0, m0, k);
+      if (!(at < m0 && (P0[at] >> 1) == (k >> 1))) ++fresh;
+    }
+  }
+  warp_add_counter(ctr, fresh);
+}
+
+// nndescent.cpp:88-99: the K nearest pool entries, flagged old, as the graph
+__global__ void __launch_bounds__(kBlock)
+    k_nd_finalize(uint64_t n, uint32_t cap, uint32_t K, const uint64_t* __restrict__ pool,
+                  const uint32_t* __restrict__ pcnt, uint64_t* __restrict__ off,
+                  uint32_t* __restrict__ cnt, uint64_t* __restrict__ key) {
+  const uint32_t lane = lane_id();
+  WARP_LOOP(u, n) {
+    const uint32_t t = pcnt[u] < K ? pcnt[u] : K;
+    for (uint32_t j = lane; j < t; j += 32) key[u * K + j] = pool[u * cap + j] & ~1ull;
+    if (lane == 0) {
+      off[u] = u * K;
+      cnt[u] = t;
+      if (u + 1 == n) off[n] = n * K;
+    }
+  }
+}
+
+}  // namespace
+
+void op_nnd_init(rnndg_ctx* c, uint32_t K, uint32_t sample, uint32_t iters, uint32_t pool,
+                 uint64_t seed) {
+  const uint64_t n = c->n;
+  if (c->partitioned) throw ParamError("nndescent: not available on a partitioned context");
+  // NnDescent::NnDescent, nndescent.cpp:11-22
+  if (n < 2) throw ParamError("nndescent: need at least 2 vectors");
+  if (K < 1 || K > n - 1) throw ParamError("nndescent: K out of [1, n-1]");
+  if (sample < 1) throw ParamError("nndescent: sample must be >= 1");
+  if (iters < 1) throw ParamError("nndescent: iters must be >= 1");
+  const uint32_t cap = std::max(pool ? pool : 2 * K, K);
+  c->nd_K = K;
+  c->nd_cap = cap;
+  c->nd_sample = sample;
+  c->nd_iters = iters;
+  // init, :24-37: the random_init sampler with s = min(sample, n - 1) ids
+  const uint32_t s = uint32_t(std::min<uint64_t>(sample, n - 1));
+  c->nd_stride = std::max(cap, s);  // pools may start above the cap
+  op_random_init(c, s, seed);
+  c->nd_pool.ensure(n * c->nd_stride);
+  c->nd_pcnt.ensure(n);
+  RNNDG_LAUNCH(c, k_nd_from_lists, warp_grid(c, n), kBlock, 0, n, c->nd_stride, c->off.p,
+               c->cnt.p, c->key.p, c->nd_pool.p, c->nd_pcnt.p);
+  c->nd_ready = true;
+}
+
+uint64_t op_nnd_pass(rnndg_ctx* c) {
+  if (!c->nd_ready) throw ParamError("nndescent: call init first");
+  const uint64_t n = c->n;
+  const uint32_t cap = c->nd_stride, sample = c->nd_sample;  // cap: the pool stride here
+  c->nd_pool0.ensure(n * cap);
+  c->nd_pcnt0.ensure(n);
+  c->nd_F.ensure(n * sample);
+  c->nd_fcnt.ensure(n);
+  c->nd_O.ensure(n * cap);
+  c->nd_ocnt.ensure(n);
+  c->nd_np.ensure(n + 1);
+  c->nd_poff.ensure(n + 1);
+  RNNDG_LAUNCH(c, k_nd_snapshot, grid_for(n, 128), 128, 0, n, cap, sample, c->nd_pool.p,
+               c->nd_pcnt.p, c->nd_F.p, c->nd_fcnt.p, c->nd_O.p, c->nd_ocnt.p, c->nd_pool0.p,
+               c->nd_pcnt0.p, c->nd_np.p);
+  scan_u32(c, c->nd_np.p, c->nd_poff.p, n);
+  std::vector<uint64_t> poff(n + 1);
+  RNNDG_CUDA(cudaMemcpyAsync(poff.data(), c->nd_poff.p, (n + 1) * 8, cudaMemcpyDeviceToHost,
+                             c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  c->nd_bcnt.ensure(n + 1);
+  c->nd_cur.ensure(n);
+  c->nd_boff.ensure(n + 1);
+  // pairs per join chunk (RNNDG_NND_CHUNK overrides, e.g. to test chunking)
+  static const uint64_t chunk_pairs = [] {
+    const char* e = std::getenv("RNNDG_NND_CHUNK");
+    const long long v = e ? std::atoll(e) : 0;
+    return v > 0 ? uint64_t(v) : kNndChunkPairs;
+  }();
+  for (uint64_t u0 = 0; u0 < n;) {
+    // the largest vertex range whose pairs fit one chunk (at least one vertex)
+    uint64_t u1 = u0 + 1;
+    {
+      uint64_t lo = u0 + 1, hi = n;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi + 1) / 2;
+        if (poff[mid] - poff[u0] <= chunk_pairs)
+          lo = mid;
+        else
+          hi = mid - 1;
+      }
+      u1 = lo;
+    }
+    const uint64_t npairs = poff[u1] - poff[u0];
+    if (npairs) {
+      const uint64_t m = 2 * npairs;
+      c->nd_pdst.ensure(m);
+      c->nd_pkey.ensure(m);
+      launch_nnd_join(c, u0, u1, npairs);
+      zero(c, c->nd_bcnt.p, n + 1);
+      RNNDG_LAUNCH(c, k_nd_count_dst, grid_for(m, 256, 148 * 64), 256, 0, m, c->nd_pdst.p,
+                   c->nd_bcnt.p);
+      RNNDG_LAUNCH(c, k_nd_seg_len, grid_for(n, 256, 148 * 64), 256, 0, n, c->nd_pcnt.p,
+                   c->nd_bcnt.p, c->nd_bcnt.p);
+      scan_u64(c, c->nd_bcnt.p, c->nd_boff.p, n);
+      const uint64_t total = read_u64(c, c->nd_boff.p + n);
+      c->nd_seg.ensure(total);
+      c->nd_seg_s.ensure(total);
+      RNNDG_LAUNCH(c, k_nd_seg_fill, warp_grid(c, n), kBlock, 0, n, cap, c->nd_pool.p,
+                   c->nd_pcnt.p, c->nd_boff.p, c->nd_seg.p, c->nd_cur.p);
+      RNNDG_LAUNCH(c, k_nd_scatter, grid_for(m, 256, 148 * 64), 256, 0, m, c->nd_pdst.p,
+                   c->nd_pkey.p, c->nd_boff.p, c->nd_cur.p, c->nd_seg.p);
+      seg_sort_keys(c, c->nd_seg.p, c->nd_seg_s.p, total, n, c->nd_boff.p, c->nd_boff.p + 1);
+      RNNDG_LAUNCH(c, k_nd_merge, warp_grid(c, n), kBlock, 0, n, c->nd_cap, cap, c->nd_boff.p,
+                   c->nd_seg_s.p, c->nd_pcnt0.p, c->nd_pool.p, c->nd_pcnt.p);
+    }
+    u0 = u1;
+  }
+  unsigned long long* ctr = c->counters.p;
+  c->counters.ensure(kNumCounters);
+  ctr = c->counters.p;
+  zero(c, ctr, 1);
+  RNNDG_LAUNCH(c, k_nd_count_new, warp_grid(c, n), kBlock, 0, n, cap, c->nd_pool.p,
+               c->nd_pcnt.p, c->nd_pool0.p, c->nd_pcnt0.p, ctr);
+  unsigned long long h = 0;
+  RNNDG_CUDA(cudaMemcpyAsync(&h, ctr, 8, cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  return h;
+}
+
+void op_nnd_finalize(rnndg_ctx* c) {
+  if (!c->nd_ready) throw ParamError("nndescent: call init first");
+  const uint64_t n = c->n;
+  const uint32_t K = c->nd_K;
+  c->off.ensure(n + 1);
+  c->cnt.ensure(n + 1);
+  c->key.ensure(n * K);
+  c->span = n * K;
+  RNNDG_LAUNCH(c, k_nd_finalize, warp_grid(c, n), kBlock, 0, n, c->nd_stride, K, c->nd_pool.p,
+               c->nd_pcnt.p, c->off.p, c->cnt.p, c->key.p);
+  c->has_graph = true;
+  c->has_distances = true;
+  c->exact_dists = true;
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+#undef WARP_LOOP
 
 }  // namespace rnndg

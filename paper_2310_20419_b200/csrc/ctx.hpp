@@ -119,6 +119,14 @@ struct rnndg_ctx {
   rnndg::DevBuf<uint32_t> post_cnt;
   rnndg::DevBuf<unsigned long long> counters;
   rnndg::DevBuf<unsigned int> work;
+  // NN-Descent baseline (build.cu, nndescent section): pools of capacity
+  // nd_cap per vertex (dense n x cap keys, sorted), the pass snapshot and
+  // the proposal / segment scratch of a join chunk
+  uint32_t nd_K = 0, nd_cap = 0, nd_stride = 0, nd_sample = 0, nd_iters = 0;
+  bool nd_ready = false;
+  rnndg::DevBuf<uint64_t> nd_pool, nd_pool0, nd_poff, nd_pkey, nd_seg, nd_seg_s, nd_boff;
+  rnndg::DevBuf<uint32_t> nd_pcnt, nd_pcnt0, nd_F, nd_fcnt, nd_O, nd_ocnt, nd_np, nd_pdst;
+  rnndg::DevBuf<unsigned long long> nd_bcnt, nd_cur;
   // dense CSR staging for rnndg_get_graph (device-side compaction)
   rnndg::DevBuf<uint64_t> ex_off;
   rnndg::DevBuf<uint32_t> ex_ids;
@@ -176,6 +184,11 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order);
 void op_sort_lists(rnndg_ctx* c);
 void op_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end);
 uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial);
+// NN-Descent baseline (nndescent.cpp, canonical deferred join)
+void op_nnd_init(rnndg_ctx* c, uint32_t K, uint32_t sample, uint32_t iters, uint32_t pool,
+                 uint64_t seed);
+uint64_t op_nnd_pass(rnndg_ctx* c);
+void op_nnd_finalize(rnndg_ctx* c);
 void op_load_fvecs(rnndg_ctx* c, const char* path, uint64_t* n, uint32_t* d);
 // dense CSR (graph.hpp view) of the owned lists into host arrays (any may be
 // null); returns the edge count

@@ -611,6 +611,63 @@ __global__ void __launch_bounds__(256) k_init_dists(uint64_t nv, uint64_t v0, ui
   }
 }
 
+// NN-Descent local join (nndescent.cpp:72-80) for vertices [u0, u1): a quad
+// per pair on the chain-blocked rows.  Pair p of vertex u (flat index
+// poff[u] + local) is fresh x fresh (i < j) for local < f(f-1)/2, else
+// fresh x old; both directed proposals (a <- b, b <- a) are written.
+__global__ void __launch_bounds__(256)
+    k_nd_join(uint64_t u0, uint64_t u1, const uint64_t* __restrict__ poff,
+              const uint32_t* __restrict__ F, const uint32_t* __restrict__ fcnt,
+              const uint32_t* __restrict__ O, const uint32_t* __restrict__ ocnt, uint32_t sample,
+              uint32_t cap, Row row, uint32_t* __restrict__ pdst, uint64_t* __restrict__ pkey) {
+  const uint32_t lane = lane_id(), quad = lane >> 2, chain = lane & 3;
+  const uint64_t p_base = poff[u0], total = poff[u1] - p_base;
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  for (uint64_t q0 = warp * 8; q0 < total; q0 += nwarps * 8) {
+    const uint64_t q = q0 + quad;
+    const bool has = q < total;
+    const uint64_t p = p_base + (has ? q : q0);
+    // vertex: last u in [u0, u1) with poff[u] <= p
+    uint64_t lo = u0, hi = u1;
+    while (hi - lo > 1) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (poff[mid] <= p)
+        lo = mid;
+      else
+        hi = mid;
+    }
+    const uint64_t u = lo;
+    const uint32_t fc = fcnt[u];
+    const uint64_t local = p - poff[u];
+    const uint64_t tri = uint64_t(fc) * (fc ? fc - 1 : 0) / 2;
+    uint32_t a, b;
+    if (local < tri) {
+      uint32_t i = 0;
+      uint64_t r = local;
+      while (r >= fc - 1 - i) {
+        r -= fc - 1 - i;
+        ++i;
+      }
+      a = F[u * sample + i];
+      b = F[u * sample + i + 1 + uint32_t(r)];
+    } else {
+      const uint64_t r = local - tri;
+      const uint32_t oc = ocnt[u];
+      a = F[u * sample + uint32_t(r / oc)];
+      b = O[u * cap + uint32_t(r % oc)];
+    }
+    const float d = quad_l2(row.xp + uint64_t(a) * row.stride, row.xp + uint64_t(b) * row.stride,
+                            chain, row.nblk, row.ntail);
+    if (has && chain == 0) {
+      pdst[2 * q] = a;
+      pkey[2 * q] = make_key(d, b, 1u);
+      pdst[2 * q + 1] = b;
+      pkey[2 * q + 1] = make_key(d, a, 1u);
+    }
+  }
+}
+
 }  // namespace
 
 ScanConfig scan_config(rnndg_ctx* c) {
@@ -634,6 +691,19 @@ void launch_init_dists(rnndg_ctx* c, uint32_t S) {
   const uint64_t cap = uint64_t(sm_count(c)) * 8;
   if (blocks > cap) blocks = cap;
   RNNDG_LAUNCH(c, k_init_dists, unsigned(blocks), 256, 0, c->nv, c->v0, S, row, c->key.p);
+}
+
+void launch_nnd_join(rnndg_ctx* c, uint64_t u0, uint64_t u1, uint64_t npairs) {
+  if (!npairs) return;
+  const ScanConfig cfg = scan_config(c);
+  prepare_chain_layout(c);
+  const Row row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail};
+  uint64_t blocks = (npairs + 63) / 64;  // 8 warps x 8 pairs
+  const uint64_t cap = uint64_t(sm_count(c)) * 8;
+  if (blocks > cap) blocks = cap;
+  RNNDG_LAUNCH(c, k_nd_join, unsigned(blocks), 256, 0, u0, u1, c->nd_poff.p, c->nd_F.p,
+               c->nd_fcnt.p, c->nd_O.p, c->nd_ocnt.p, c->nd_sample, c->nd_stride, row, c->nd_pdst.p,
+               c->nd_pkey.p);
 }
 
 void prepare_chain_layout(rnndg_ctx* c) {

@@ -26,5 +26,9 @@ void launch_scan(rnndg_ctx* c, unsigned int* work);
 // cached distances of the random initial lists (k_random_init left the raw
 // samples in the keys' low 32 bits)
 void launch_init_dists(rnndg_ctx* c, uint32_t S);
+// NN-Descent join of vertices [u0, u1): every pair of their snapshot lists
+// (fresh x fresh, fresh x old; pair p of vertex u at poff[u] + local index)
+// proposes each endpoint to the other, written at 2 * (p - poff[u0])
+void launch_nnd_join(rnndg_ctx* c, uint64_t u0, uint64_t u1, uint64_t npairs);
 
 }  // namespace rnndg

@@ -433,6 +433,89 @@ def build(store: VectorStore, params: BuildParams = BuildParams(),
     return g
 
 
+@dataclass
+class NnDescentParams:
+    """nndescent.hpp:12-19"""
+
+    K: int = 64
+    sample: int = 10
+    iters: int = 10
+    pool: int = 0  # 0 selects 2 * K
+    seed: int = kDefaultSeed
+    threads: int = 0  # accepted, ignored (the device join is deterministic)
+
+
+class NnDescent:
+    """nndescent.hpp:27-47 on the GPU, canonical deferred join: each pass
+    snapshots every pool, joins all pairs, then keeps the `cap` nearest
+    distinct entries of pool + proposals (include/rnndg.h rnndg_nnd_*).  The
+    reference's own join is order-dependent for threads > 1."""
+
+    def __init__(self, store, params: NnDescentParams = NnDescentParams(),
+                 device: Optional[Device] = None):
+        if isinstance(store, DeviceStore):
+            device = store.device
+        self.dev = device or Device()
+        if self.dev.store_ref is not store:
+            self.dev.set_data(store)
+        self.store = store
+        self.params = params
+        self._initialised = False
+
+    def init(self):
+        p = self.params
+        self.dev.check(self.dev._L.rnndg_nnd_init(self.dev.h, p.K, p.sample, p.iters, p.pool,
+                                                  p.seed))
+        self._initialised = True
+
+    def join_pass(self) -> int:
+        """Returns the number of entries new to the pools."""
+        m = C.c_uint64()
+        self.dev.check(self.dev._L.rnndg_nnd_pass(self.dev.h, C.byref(m)))
+        return int(m.value)
+
+    def pools(self) -> List[List[NeighborEntry]]:
+        cap = C.c_uint32()
+        self.dev.check(self.dev._L.rnndg_nnd_pools(self.dev.h, C.byref(cap), None, None, None,
+                                                   None))
+        n, k = self.store.n, int(cap.value)
+        cnt = np.zeros(n, np.uint32)
+        ids = np.zeros(n * k, np.uint32)
+        ds = np.zeros(n * k, np.float32)
+        fr = np.zeros(n * k, np.uint8)
+        self.dev.check(self.dev._L.rnndg_nnd_pools(self.dev.h, C.byref(cap), ptr(cnt, u32p),
+                                                   ptr(ids, u32p), ptr(ds, f32p), ptr(fr, u8p)))
+        return [[NeighborEntry(int(ids[u * k + j]), float(ds[u * k + j]), bool(fr[u * k + j]))
+                 for j in range(int(cnt[u]))] for u in range(n)]
+
+    def finalize(self) -> "AdjacencyGraph":
+        self.dev.check(self.dev._L.rnndg_nnd_finalize(self.dev.h))
+        g = AdjacencyGraph(self.store.n)
+        g._dev, g._dev_fresh, g.has_distances = self.dev, True, True
+        return g
+
+
+def build_nndescent(store, params: NnDescentParams = NnDescentParams(),
+                    stats: Optional[BuildStats] = None,
+                    device: Optional[Device] = None) -> "AdjacencyGraph":
+    """nndescent.cpp:101-119 on the GPU (canonical deferred join)."""
+    if isinstance(store, DeviceStore):
+        device = store.device
+    dev = device or Device()
+    if dev.store_ref is not store:
+        dev.set_data(store)
+    st = _lib.BuildStatsC()
+    dev.check(dev._L.rnndg_nnd_build(dev.h, params.K, params.sample, params.iters, params.pool,
+                                     params.seed, C.byref(st)))
+    g = AdjacencyGraph(store.n)
+    g._dev, g._dev_fresh, g.has_distances = dev, True, True
+    if stats is not None:
+        stats.seconds = st.seconds
+        stats.update_passes = st.update_passes
+        stats.kernel_launches = st.kernel_launches
+    return g
+
+
 def rng_strategy(store: VectorStore, u: int, candidates: Sequence[NeighborEntry],
                  device: Optional[Device] = None) -> List[NeighborEntry]:
     """builder.cpp:196-212"""
