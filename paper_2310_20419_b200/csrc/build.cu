@@ -861,8 +861,10 @@ void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t
   if (c->trace)
     std::fprintf(stderr,
                  "[rnndg] pass active=%llu large=%llu maxlen=%llu entries=%llu checks=%llu "
-                 "removed=%llu inserted=%llu touched=%llu order=%.3fms scan=%.3fms apply=%.3fms\n",
+                 "evals=%llu hub_evals=%llu removed=%llu inserted=%llu touched=%llu "
+                 "order=%.3fms scan=%.3fms apply=%.3fms\n",
                  h[kActiveCount], h[kLargeCount], h[kMaxLen], h[kActiveEntries], h[kPairChecks],
+                 h[kEvalPairs], h[kEvalHub],
                  h[kRemoved], h[kInserted], h[kTouched], elapsed_ms(c->ev[0], c->ev[1]),
                  elapsed_ms(c->ev[1], c->ev[2]), elapsed_ms(c->ev[2], c->ev[3]));
 }

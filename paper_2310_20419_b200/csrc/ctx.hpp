@@ -74,6 +74,8 @@ enum Counter : int {
   kActiveCount,
   kLargeCount,
   kMaxLen,
+  kEvalPairs,  // distances evaluated by the scan (incl. speculative ones)
+  kEvalHub,    // ... of which by the hub-list kernel
   kNumCounters
 };
 

@@ -421,7 +421,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   const Row row = g.row;
   const uint32_t row_bytes = row.stride * 4u;
   const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount]) : uint32_t(*g.nsmall);
-  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, evals = 0;
 
   for (;;) {
     if (tid == 0) s_a = atomicAdd(g.work + (kLong ? 1 : 0), 1u);
@@ -469,6 +469,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
           if (uint32_t(i) < lim && (key_fresh(wk[i]) || vf)) nm |= 1u << i;
         uint32_t ntask;
         const uint32_t tb = block_excl_scan<W>(__popc(nm), wcnt, ntask);
+        evals += tid == 0 ? ntask : 0u;
         {
           uint32_t t = tb;
 #pragma unroll
@@ -587,6 +588,10 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
     __syncthreads();
   }
   flush_counters(g.ctr, removed, checks, skips, touched);
+  if (tid == 0 && evals) {
+    atomicAdd(&g.ctr[kEvalPairs], evals);
+    if (kLong) atomicAdd(&g.ctr[kEvalHub], evals);
+  }
 }
 
 // Cached distances of the random initial lists (graph.cpp:53-61), a quad per
