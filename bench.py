@@ -51,6 +51,18 @@ def parse():
     return ap.parse_args()
 
 
+_STDOUT_FD = None
+
+
+def print_line(line: dict):
+    """The one JSON line, on the real stdout even if fd 1 was redirected."""
+    sys.stdout.flush()
+    if _STDOUT_FD is not None:
+        os.write(_STDOUT_FD, (json.dumps(line) + "\n").encode())
+    else:
+        print(json.dumps(line), flush=True)
+
+
 def dist_env():
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -282,7 +294,7 @@ def run_sharded(args, rank, world, local):
             "gpu_launches": int(vals[3]) * world,
             "clocks": clk.summary(),
         }
-        print(json.dumps(line))
+        print_line(line)
 
 
 def main():
@@ -295,6 +307,12 @@ def main():
     import torch
     torch.cuda.set_device(local)
     if world > 1 or args.sharded:
+        # NCCL / c10d print banners on stdout; keep stdout for the one JSON
+        # line (run_sharded restores it to print)
+        global _STDOUT_FD
+        sys.stdout.flush()
+        _STDOUT_FD = os.dup(1)
+        os.dup2(2, 1)
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")

@@ -86,12 +86,13 @@ class TorchDistTransport:
         self.dist.all_to_all_single(rc, sc, group=self.group)
         rcl = [int(x) for x in rc.tolist()]
         scl = [int(x) for x in sc.tolist()]
-        # one collective for both fields: record i = (dst widened, key) as int64
-        send = torch.stack([dst.to(torch.int64), key.to(torch.int64)], dim=1).contiguous()
-        recv = torch.empty((sum(rcl), 2), dtype=torch.int64, device=dev)
-        self.dist.all_to_all_single(recv, send, output_split_sizes=rcl, input_split_sizes=scl,
+        rdst = torch.empty(sum(rcl), dtype=dst.dtype, device=dev)
+        rkey = torch.empty(sum(rcl), dtype=key.dtype, device=dev)
+        self.dist.all_to_all_single(rdst, dst, output_split_sizes=rcl, input_split_sizes=scl,
                                     group=self.group)
-        return [(recv[:, 0].to(dst.dtype).contiguous(), recv[:, 1].contiguous())]
+        self.dist.all_to_all_single(rkey, key, output_split_sizes=rcl, input_split_sizes=scl,
+                                    group=self.group)
+        return [(rdst, rkey)]
 
     def allreduce(self, vals):
         import torch
