@@ -164,10 +164,11 @@ def run_reference(args, rank, world):
         "impl": "reference", "metric": METRIC, "value": value, "unit": "dist-evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded generator, csrc/datagen.cpp)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded generator, csrc/datagen.cpp; stands in for GIST1M)",
         "config": {"workload": cfg.name, "rows": cfg.n, "dim": cfg.d, "sample_rows": n,
-                   "S": 20, "R": 96, "T1": 4, "T2": 15},
+                   "S": 20, "R": 96, "T1": 4, "T2": 15,
+                   "parallelism": f"host threads x{cores} (rank 0 only)"},
         "cpu_baseline": {"value": value, "unit": "dist-evals/s", "cores": cores,
                          "kind": "reference",
                          "sample": f"rnnd::build(threads={cores}) on the first {n} rows of "
