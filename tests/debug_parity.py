@@ -1,11 +1,11 @@
-"""Debug helper: run update passes on the GPU and the oracle side by side and
+"""Debug helper (test infrastructure; imports the oracle): run update passes on the GPU and the oracle side by side and
 print the first divergence (counts, then the first differing vertex)."""
 import ctypes as C
 import sys
 
 import numpy as np
 
-sys.path.insert(0, __file__.rsplit("/tools/", 1)[0])
+sys.path.insert(0, __file__.rsplit("/tests/", 1)[0])
 from oracle import oracle as O  # noqa: E402
 from paper_2310_20419_b200 import _lib  # noqa: E402
 from paper_2310_20419_b200 import rnnd as R  # noqa: E402

@@ -5,7 +5,7 @@ import sys
 
 import numpy as np
 
-ROOT = __file__.rsplit("/tools/", 1)[0]
+ROOT = __file__.rsplit("/tests/", 1)[0]
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 from shard_cpu import CpuShard  # noqa: E402
