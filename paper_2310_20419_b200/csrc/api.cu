@@ -79,6 +79,7 @@ int rnndg_create(rnndg_ctx** out, int device) {
     RNNDG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     RNNDG_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     for (auto& e : c->ev) RNNDG_CUDA(cudaEventCreate(&e));
+    for (auto& e : c->ev_scan) RNNDG_CUDA(cudaEventCreate(&e));
     const char* tr = std::getenv("RNNDG_TRACE");
     c->trace = tr && tr[0] == '1';
   } catch (const ParamError&) {
@@ -97,6 +98,8 @@ int rnndg_destroy(rnndg_ctx* c) {
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   for (auto& e : c->ev)
+    if (e) cudaEventDestroy(e);
+  for (auto& e : c->ev_scan)
     if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamSynchronize(c->side);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);

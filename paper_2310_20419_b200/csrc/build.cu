@@ -125,10 +125,11 @@ __global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
                               uint8_t* __restrict__ active,
                               uint32_t* __restrict__ act_list,
                               uint32_t* __restrict__ post_cnt,
-                              unsigned long long* __restrict__ ctr, uint32_t ucap) {
+                              unsigned long long* __restrict__ ctr, uint32_t ucap,
+                              uint32_t big_cap) {
   const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
   unsigned long long skips = 0, aentries = 0, nact = 0;
-  bool large = false;
+  bool large = false, big = false;
   if (u < n) {
     const uint64_t b = off[u];
     const uint32_t U = cnt[u];
@@ -142,8 +143,9 @@ __global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
     if (act) {
       aentries = U;
       nact = 1;
-      large = U > ucap;
-      flag = large ? 2 : 1;
+      big = U > big_cap;
+      large = U > ucap && !big;
+      flag = U > ucap ? 2 : 1;
       atomicMax(&ctr[kMaxLen], (unsigned long long)U);
     } else {
       post_cnt[u] = U;
@@ -157,6 +159,13 @@ __global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
     bl = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLargeCount]), __popc(ml));
   bl = __shfl_sync(0xffffffffu, bl, 0);
   if (large) act_list[n + bl + __popc(ml & ((1u << lane_id()) - 1))] = uint32_t(u);
+  // lists longer than big_cap are queued from the end, act_list[2n - 1 - i]
+  const unsigned mb = __ballot_sync(0xffffffffu, big);
+  uint32_t bb = 0;
+  if (lane_id() == 0 && mb)
+    bb = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kBigCount]), __popc(mb));
+  bb = __shfl_sync(0xffffffffu, bb, 0);
+  if (big) act_list[2 * n - 1 - (bb + __popc(mb & ((1u << lane_id()) - 1)))] = uint32_t(u);
   warp_add_counter(&ctr[kFlagSkips], skips);
   warp_add_counter(&ctr[kActiveEntries], aentries);
   warp_add_counter(&ctr[kActiveCount], nact);
@@ -669,7 +678,7 @@ void ensure_scratch(rnndg_ctx* c) {
   c->bcur.ensure(n);
   c->boff.ensure(n + 1);
   c->counters.ensure(kNumCounters);
-  c->work.ensure(4);
+  c->work.ensure(8);
   c->label.ensure(2 * n);
   c->okey.ensure(2 * n);
   c->act_small.ensure(n);
@@ -714,6 +723,23 @@ uint32_t hub_threshold() {
     const char* e = std::getenv("RNNDG_UCAP");
     const int x = e ? std::atoi(e) : 256;
     return uint32_t(x >= 32 && x <= int(kScanUcap) ? x : 256);
+  }();
+  return v;
+}
+
+// hub lists longer than this are walked by a whole thread-block cluster
+// (k_scan_hub phase 1); shorter hubs by one CTA each (RNNDG_BIG_HUB; 0 = no
+// cooperative walks)
+uint32_t big_hub_threshold() {
+  static const uint32_t v = [] {
+    // the one-CTA-per-hub fallbacks (RNNDG_HUB=0, RNNDG_SPEC=0) have no
+    // cooperative phase
+    const char* h = std::getenv("RNNDG_HUB");
+    const char* sp = std::getenv("RNNDG_SPEC");
+    if ((h && std::atoi(h) == 0) || (sp && std::atoi(sp) == 0)) return 0xFFFFFFFFu;
+    const char* e = std::getenv("RNNDG_BIG_HUB");
+    const long x = e ? std::atol(e) : 1024;
+    return x <= 0 ? 0xFFFFFFFFu : uint32_t(x < 256 ? 256 : x);
   }();
   return v;
 }
@@ -811,7 +837,7 @@ void op_scan_phase(rnndg_ctx* c) {
   ensure_scratch(c);
   unsigned long long* ctr = c->counters.p;
   zero(c, ctr, kNumCounters);
-  zero(c, c->work.p, 4);
+  zero(c, c->work.p, 8);
   zero(c, c->pend_src.p, c->span, 0xFF);
   zero(c, c->touch.p, c->span);
   zero(c, c->bcnt.p, n + 1);
@@ -819,7 +845,8 @@ void op_scan_phase(rnndg_ctx* c) {
   RNNDG_CUDA(cudaEventRecord(c->ev[0], c->stream));
   if (n)
     RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
-                 c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold());
+                 c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
+                 big_hub_threshold());
   locality_order(c);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
   launch_scan(c, c->work.p);
@@ -862,11 +889,12 @@ void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t
     std::fprintf(stderr,
                  "[rnndg] pass active=%llu large=%llu maxlen=%llu entries=%llu checks=%llu "
                  "evals=%llu hub_evals=%llu removed=%llu inserted=%llu touched=%llu "
-                 "order=%.3fms scan=%.3fms apply=%.3fms\n",
-                 h[kActiveCount], h[kLargeCount], h[kMaxLen], h[kActiveEntries], h[kPairChecks],
+                 "order=%.3fms scan=%.3fms apply=%.3fms hubk=%.3fms shortk=%.3fms\n",
+                 h[kActiveCount], h[kLargeCount] + h[kBigCount], h[kMaxLen], h[kActiveEntries], h[kPairChecks],
                  h[kEvalPairs], h[kEvalHub],
                  h[kRemoved], h[kInserted], h[kTouched], elapsed_ms(c->ev[0], c->ev[1]),
-                 elapsed_ms(c->ev[1], c->ev[2]), elapsed_ms(c->ev[2], c->ev[3]));
+                 elapsed_ms(c->ev[1], c->ev[2]), elapsed_ms(c->ev[2], c->ev[3]),
+                 elapsed_ms(c->ev[1], c->ev_scan[0]), elapsed_ms(c->ev[1], c->ev_scan[1]));
 }
 
 uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,

@@ -76,6 +76,7 @@ enum Counter : int {
   kMaxLen,
   kEvalPairs,  // distances evaluated by the scan (incl. speculative ones)
   kEvalHub,    // ... of which by the hub-list kernel
+  kBigCount,   // hub lists longer than big_hub_threshold() (cluster-cooperative)
   kNumCounters
 };
 
@@ -161,6 +162,7 @@ struct rnndg_ctx {
   uint64_t shard_touched = 0, shard_active = 0, shard_passes = 0;
   // timing events
   cudaEvent_t ev[8] = {};
+  cudaEvent_t ev_scan[2] = {};  // trace only: hub kernel end (side), short kernel end (main)
 };
 
 namespace rnndg {

@@ -25,8 +25,12 @@
 //
 //   k_scan_spec<2, false, 4>   lists <= hub_threshold() (256): keys + alive
 //                              list in smem, 7 CTAs of 64 threads per SM
-//   k_scan_spec<32, true, 4>   hub lists, 1024-thread CTAs on every SM, on a
-//                              second stream concurrently
+//   k_scan_hub<32, 2, 4>       hub lists, on a second stream concurrently:
+//                              clusters of two 1024-thread CTAs; lists over
+//                              big_hub_threshold() (1024) walked by both CTAs
+//                              of a cluster (longest first), the rest by one
+//   k_scan_spec<32, true, 4>   hub lists, one 1024-thread CTA each
+//                              (RNNDG_HUB=0)
 //   k_scan_block               the same walk with two steps per round
 //                              (RNNDG_SPEC=0)
 // Variants measured slower and removed (smem-staged rows, TMA-sliced rows, a
@@ -34,6 +38,8 @@
 // tasks, early exit, deeper register pipelines): profiles/README.md.
 #include <cstdio>
 #include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "ctx.hpp"
@@ -594,6 +600,381 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   }
 }
 
+// ------------------------------------------------------------ hub clusters
+// k_scan_spec's walk for hub lists, spread over a thread-block cluster of C
+// CTAs (one hub per cluster, persistent over the hub queue).  The single
+// 1024-thread CTA per hub left the passes after each reverse phase bound by
+// the largest hub's walk (one CTA's quads against a 5-10k-entry list).
+//
+// CTA r owns the list positions p with p % C == r and keeps its own alive
+// list (ascending positions) in its slice of global scratch alive_g[base ..).
+// A round: every CTA publishes its first D alive positions and its alive
+// count in shared memory; after one cluster barrier every CTA merges the C*D
+// heads over DSMEM into the same w_1..w_D (the D smallest alive positions of
+// the whole list), pops the ones it owns, and tests its remaining alive
+// candidates -- all of which come after w_D in list order -- against them.
+// The fates of w_2..w_D (pairs among the w's only) are evaluated by every CTA
+// redundantly, so each knows the kept mask without another exchange; the
+// owner of w_j does w_j's bookkeeping (counters, redirect).  Kept entries of
+// round r are written to L[nk..] by rank 0 after the next round's barrier,
+// when no CTA reads round r's keys any more.  The head buffers are
+// double-buffered by round parity, so one cluster barrier per round suffices.
+// Pairs, counters and redirects are exactly k_scan_spec's.
+template <int W, int D>
+struct HubSmem {
+  static constexpr uint32_t kTasks = 32 * W * D + D * (D - 1) / 2;
+  uint32_t tq[kTasks];
+  uint8_t tw[kTasks];
+  float tres[kTasks];
+  uint32_t wcnt[W];
+  uint32_t head[2][D];
+  uint32_t na[2];
+  uint32_t a, tot, kept, npk;
+  uint32_t wp[D];
+  uint32_t tb[D], nm[D];  // fate tasks of w_2 .. w_D
+  uint64_t pk[D];         // kept keys of the previous round (rank 0)
+};
+
+struct HubCounters {
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, evals = 0;
+};
+
+// The walk of one hub list u by `cs` cooperating CTAs (cs == C, the cluster,
+// for lists longer than big_hub_threshold(); cs == 1, this CTA alone,
+// otherwise).  rank = this CTA's rank among them.
+template <int W, int D>
+__device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t cs, uint32_t rank,
+                                         HubSmem<W, D>& sm, HubCounters& hc) {
+  namespace cg = cooperative_groups;
+  constexpr uint32_t NT = 32 * W;
+  constexpr uint32_t kInf = 0xFFFFFFFFu;
+  cg::cluster_group cl = cg::this_cluster();
+  const bool coop = cs > 1;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
+  const uint32_t quad = lane >> 2, chain = lane & 3;
+  const Row row = g.row;
+  const uint32_t row_bytes = row.stride * 4u;
+  const uint64_t base = g.off[u];
+  const uint32_t U = g.cnt[u];
+  uint64_t* L = g.keys + base;
+  uint8_t* T = g.touch + base;
+  // rank r owns positions p % cs == r: U / cs of them, plus one while r < U % cs
+  uint32_t* A = g.alive_g + base + rank * (U / cs) + (rank < U % cs ? rank : U % cs);
+  uint32_t na = U / cs + (rank < U % cs ? 1u : 0u);
+  for (uint32_t i = tid; i < na; i += NT) {
+    const uint32_t p = rank + i * cs;
+    A[i] = p;
+    prefetch_row_l2(row(L[p]), row_bytes);
+  }
+  if (tid == 0) sm.npk = 0;
+  __syncthreads();
+  uint32_t nk = 0, ao = 0;
+  for (uint32_t rnd = 0;; ++rnd) {
+    const uint32_t buf = rnd & 1u;
+    if (tid < uint32_t(D)) sm.head[buf][tid] = tid < na ? A[ao + tid] : kInf;
+    if (tid == 0) sm.na[buf] = na;
+    if (coop)
+      cl.sync();
+    else
+      __syncthreads();
+    if (rank == 0 && tid == 0)
+      for (uint32_t i = 0; i < sm.npk; ++i) L[nk - sm.npk + i] = sm.pk[i];
+    if (wid == 0) {
+      // D smallest of the cs*D published heads, and the total alive count
+      uint32_t h0 = kInf, h1 = kInf, cnt = 0;
+      if (coop) {
+        if (lane < cs * D) h0 = cl.map_shared_rank(&sm.head[buf][0], lane / D)[lane % D];
+        if (lane + 32 < cs * D)
+          h1 = cl.map_shared_rank(&sm.head[buf][0], (lane + 32) / D)[(lane + 32) % D];
+        if (lane < cs) cnt = *cl.map_shared_rank(&sm.na[buf], lane);
+      } else {
+        if (lane < uint32_t(D)) h0 = sm.head[buf][lane];
+        if (lane == 0) cnt = sm.na[buf];
+      }
+      const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
+#pragma unroll
+      for (int i = 0; i < D; ++i) {
+        const uint32_t m = __reduce_min_sync(0xffffffffu, h0 < h1 ? h0 : h1);
+        if (h0 == m) h0 = kInf;
+        if (h1 == m) h1 = kInf;
+        if (lane == 0) sm.wp[i] = m;
+      }
+      if (lane == 0) sm.tot = tot;
+    }
+    __syncthreads();
+    const uint32_t tot = sm.tot;
+    if (tot == 0) break;
+    const uint32_t De = tot < uint32_t(D) ? tot : uint32_t(D);
+    uint64_t wk[D];
+    uint32_t wp[D];
+    uint32_t own = 0;  // w's owned by this CTA: its first `own` alive entries
+#pragma unroll
+    for (int i = 0; i < D; ++i) {
+      wp[i] = uint32_t(i) < De ? sm.wp[i] : sm.wp[0];
+      wk[i] = L[wp[i]];
+      own += (uint32_t(i) < De && wp[i] % cs == rank) ? 1u : 0u;
+    }
+    ao += own;
+    na -= own;
+    // fate tasks: w_j against w_i, i < j, where a flag is fresh
+    if (tid == 0) {
+      uint32_t t = 0;
+      for (uint32_t j = 1; j < uint32_t(D); ++j) {
+        uint32_t nm = 0;
+        if (j < De)
+          for (uint32_t i = 0; i < j; ++i)
+            if (key_fresh(wk[i]) || key_fresh(wk[j])) nm |= 1u << i;
+        sm.tb[j] = t;
+        sm.nm[j] = nm;
+        for (uint32_t i = 0; i < j; ++i)
+          if (nm >> i & 1u) {
+            sm.tq[t] = wp[j];
+            sm.tw[t] = uint8_t(i);
+            ++t;
+          }
+      }
+      sm.tb[0] = t;  // number of fate tasks
+    }
+    __syncthreads();
+    const uint32_t nf = sm.tb[0];
+    uint32_t nn = 0;  // survivors, compacted into A[0 ..)
+    uint32_t kept = 1u;
+    for (uint32_t b0 = 0; b0 == 0 || b0 < na; b0 += NT) {
+      const uint32_t ai = b0 + tid;
+      const bool valid = ai < na;
+      const uint32_t q = valid ? A[ao + ai] : 0u;
+      const uint64_t vk = valid ? L[q] : 0ull;
+      const bool vf = key_fresh(vk);
+      uint32_t nm = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+        if (valid && uint32_t(i) < De && (key_fresh(wk[i]) || vf)) nm |= 1u << i;
+      uint32_t ntask;
+      const uint32_t pre = b0 == 0 ? nf : 0u;
+      const uint32_t tb = pre + block_excl_scan<W>(__popc(nm), sm.wcnt, ntask);
+      ntask += pre;
+      hc.evals += tid == 0 ? ntask : 0u;
+      {
+        uint32_t t = tb;
+#pragma unroll
+        for (int i = 0; i < D; ++i)
+          if (nm >> i & 1u) {
+            sm.tq[t] = q;
+            sm.tw[t] = uint8_t(i);
+            ++t;
+          }
+      }
+      __syncthreads();
+      for (uint32_t t0 = 0; t0 < ntask; t0 += 8 * W) {
+        const uint32_t twp = t0 + 8 * wid;
+        if (twp >= ntask) continue;  // warp-uniform
+        const uint32_t ti = twp + quad;
+        const bool has = ti < ntask;
+        const uint32_t ts = has ? ti : twp;
+        const float* xv = row(L[sm.tq[ts]]);
+        const uint32_t wsel = sm.tw[ts];
+        uint64_t wkey = wk[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i)
+          if (wsel == uint32_t(i)) wkey = wk[i];
+        const float dist = quad_l2(xv, row(wkey), chain, row.nblk, row.ntail);
+        if (has && chain == 0) sm.tres[ti] = dist;
+      }
+      __syncthreads();
+      if (b0 == 0) {
+        // fates of w_2 .. w_De in list order; the owner of w_j books its walk
+        // exactly as k_scan_spec's candidate ai == j
+        if (tid == 0) {
+          uint32_t kb = 1u;
+          for (uint32_t j = 1; j < De; ++j) {
+            const float dj = key_dist(wk[j]);
+            const bool mine = wp[j] % cs == rank;
+            uint32_t t = sm.tb[j];
+            bool occl = false;
+            uint32_t by = 0;
+            float dvw = 0.f;
+            for (uint32_t i = 0; i < j && !occl; ++i) {
+              const bool nd = sm.nm[j] >> i & 1u;
+              const float d = nd ? sm.tres[t] : 0.f;
+              if (nd) ++t;
+              if (!(kb >> i & 1u)) continue;
+              if (!nd) {
+                if (mine) ++hc.skips;
+                continue;
+              }
+              if (mine) {
+                ++hc.checks;
+                T[wp[j]] = 1;
+                T[wp[i]] = 1;
+              }
+              if (dj >= d) {
+                occl = true;
+                by = i;
+                dvw = d;
+              }
+            }
+            if (!occl) {
+              kb |= 1u << j;
+            } else if (mine) {
+              ++hc.removed;
+              const uint32_t w_id = key_id(wk[by]);
+              g.pend_src[base + wp[j]] = w_id;
+              g.pend_key[base + wp[j]] = make_key(dvw, key_id(wk[j]), 1u);
+              if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
+            }
+          }
+          sm.kept = kb;
+        }
+        __syncthreads();
+        kept = sm.kept;
+      }
+      bool gone = false;
+      uint32_t by = 0;
+      float dvw = 0.f;
+      {
+        uint32_t t = tb;
+#pragma unroll
+        for (int i = 0; i < D; ++i) {
+          if (uint32_t(i) >= De || !valid || gone) continue;
+          const bool nd = nm >> i & 1u;
+          const float d = nd ? sm.tres[t] : 0.f;
+          if (nd) ++t;
+          if (!(kept >> i & 1u)) continue;
+          if (!nd) {
+            ++hc.skips;
+            continue;
+          }
+          ++hc.checks;
+          T[q] = 1;
+          T[wp[i]] = 1;
+          if (key_dist(vk) >= d) {
+            gone = true;
+            by = uint32_t(i);
+            dvw = d;
+          }
+        }
+      }
+      if (gone) {
+        ++hc.removed;
+        uint64_t wkey = wk[0];
+#pragma unroll
+        for (int i = 1; i < D; ++i)
+          if (by == uint32_t(i)) wkey = wk[i];
+        const uint32_t w_id = key_id(wkey);
+        g.pend_src[base + q] = w_id;
+        g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
+        if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
+      }
+      const bool stay = valid && !gone;
+      uint32_t nstay;
+      const uint32_t r = block_rank<W>(stay, sm.wcnt, nstay);
+      if (stay) A[nn + r] = q;
+      nn += nstay;
+      __syncthreads();
+    }
+    const uint32_t km = kept & ((1u << De) - 1u);
+    if (rank == 0 && tid == 0) {
+      uint32_t t = 0;
+#pragma unroll
+      for (int i = 0; i < D; ++i)
+        if (km >> i & 1u) sm.pk[t++] = wk[i] & ~1ull;
+      sm.npk = t;
+    }
+    nk += __popc(km);
+    na = nn;
+    ao = 0;
+  }
+  if (rank == 0 && tid == 0) g.post_cnt[u] = nk;
+  for (uint32_t j = rank + tid * cs; j < U; j += NT * cs) hc.touched += T[j];
+  __syncthreads();
+}
+
+// Launched as clusters of C CTAs.  Phase 1: each cluster walks the big hubs
+// (queue act_list[2n - 1 - a], a < kBigCount) cooperatively, one at a time.
+// Phase 2: every CTA walks the remaining hub lists (act_list[n + a], a <
+// kLargeCount) on its own, like k_scan_spec<32, true, 4>.
+__device__ __forceinline__ void flush_hub(const ScanArgs& g, const HubCounters& hc) {
+  flush_counters(g.ctr, hc.removed, hc.checks, hc.skips, hc.touched);
+  if (threadIdx.x == 0 && hc.evals) {
+    atomicAdd(&g.ctr[kEvalPairs], hc.evals);
+    atomicAdd(&g.ctr[kEvalHub], hc.evals);
+  }
+}
+
+constexpr uint32_t kCoopAll = 4;  // hubs per cluster below which all are cooperative
+
+template <int W, int C, int D>
+__global__ void __launch_bounds__(32 * W, 1) k_scan_hub(ScanArgs g) {
+  namespace cg = cooperative_groups;
+  static_assert(C * D <= 64, "head merge holds two heads per lane");
+  __shared__ HubSmem<W, D> sm;
+  cg::cluster_group cl = cg::this_cluster();
+  const uint32_t rank = cl.block_rank();
+  const uint32_t tid = threadIdx.x;
+  const uint32_t nbig = uint32_t(g.ctr_in[kBigCount]);
+  const uint32_t nmid = uint32_t(g.ctr_in[kLargeCount]);
+  // few hubs in all (the tail passes): every hub is walked cooperatively,
+  // the big ones (largest first, k_sort_big) before the rest
+  const bool coop_all = nbig + nmid <= kCoopAll * (gridDim.x / C);
+  const uint32_t ncoop = nbig + (coop_all ? nmid : 0u);
+  HubCounters hc;
+  for (;;) {
+    if (rank == 0 && tid == 0) sm.a = atomicAdd(g.work + 1, 1u);
+    cl.sync();
+    const uint32_t a = *cl.map_shared_rank(&sm.a, 0);
+    cl.sync();  // rank 0's sm.a is read before it moves on
+    if (a >= ncoop) break;
+    const uint32_t u = a < nbig ? g.act_list[2 * g.n - 1 - a] : g.act_list[g.n + (a - nbig)];
+    hub_walk<W, D>(g, u, C, rank, sm, hc);
+  }
+  if (coop_all) return flush_hub(g, hc);
+  // no DSMEM access past this point: CTAs may run (and exit) independently
+  for (;;) {
+    if (tid == 0) sm.a = atomicAdd(g.work + 4, 1u);
+    __syncthreads();
+    const uint32_t a = sm.a;
+    __syncthreads();
+    if (a >= nmid) break;
+    hub_walk<W, D>(g, g.act_list[g.n + a], 1, 0, sm, hc);
+  }
+  flush_hub(g, hc);
+}
+
+// Big-hub queue act_list[2n - nbig .. 2n) sorted by length, longest at
+// act_list[2n - 1] (taken first): one CTA, bitonic sort in shared memory of
+// (length, vertex) keys.  Skipped when the queue exceeds kSortBig entries
+// (throughput passes, where the order does not set the critical path).
+constexpr uint32_t kSortBig = 4096;
+__global__ void __launch_bounds__(1024) k_sort_big(uint32_t* __restrict__ act_list, uint64_t n,
+                                                  const uint32_t* __restrict__ cnt,
+                                                  const unsigned long long* __restrict__ ctr) {
+  __shared__ uint64_t k[kSortBig];
+  const uint32_t nb = uint32_t(ctr[kBigCount]);
+  if (nb < 2 || nb > kSortBig) return;
+  uint32_t m = 1;
+  while (m < nb) m <<= 1;
+  uint32_t* q = act_list + 2 * n - nb;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x)
+    k[i] = i < nb ? (uint64_t(cnt[q[i]]) << 32 | q[i]) : ~0ull;
+  __syncthreads();
+  for (uint32_t s = 2; s <= m; s <<= 1)
+    for (uint32_t j = s >> 1; j; j >>= 1) {
+      for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+        const uint32_t l = i ^ j;
+        if (l > i) {
+          const bool up = (i & s) == 0;
+          const uint64_t a = k[i], b = k[l];
+          if ((a > b) == up) {
+            k[i] = b;
+            k[l] = a;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  for (uint32_t i = threadIdx.x; i < nb; i += blockDim.x) q[i] = uint32_t(k[i]);
+}
+
 // Cached distances of the random initial lists (graph.cpp:53-61), a quad per
 // (u, id) pair on the chain-blocked rows.  key[p] holds the raw Floyd sample
 // of pair p = ul * S + j (not yet shifted past the pivot u, rng.hpp:68-70).
@@ -799,7 +1180,42 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return v == 8 || v == 16 ? v : kLongWarps;
   }();
   const unsigned long_grid = unsigned(sm_count(c)) * unsigned(kLongWarps / long_w) / long_div;
-  if (spec == 0)
+  // hub lists on thread-block clusters of 1024-thread CTAs (RNNDG_HUB = CTAs
+  // per cluster: 2 (default) or 4; 0 = k_scan_spec, one CTA per hub).  C3 1M
+  // (big-hub threshold 1024): 2 -> 2.25 s, 4 -> 2.26 s, 0 -> 2.42 s; clusters
+  // of 8 x 16 warps 2.38 s, 8 x 8 warps 2.41 s, 4 x 4 warps 2.36 s.
+  static const int hub_mode = [] {
+    const char* e = std::getenv("RNNDG_HUB");
+    const int v = e ? std::atoi(e) : 2;
+    return v == 0 || v == 4 ? v : 2;
+  }();
+  if (spec != 0 && hub_mode != 0) {
+    auto khub = hub_mode == 4 ? k_scan_hub<kLongWarps, 4, kSpec> : k_scan_hub<kLongWarps, 2, kSpec>;
+    const int hc = hub_mode, hw = kLongWarps;
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute attr{};
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = unsigned(hc);
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.gridDim = dim3(unsigned(hc) * 64u);
+    cfg.blockDim = dim3(32u * unsigned(hw));
+    cfg.stream = c->side;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    static int max_clusters = 0;
+    if (!max_clusters) {
+      RNNDG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, khub, &cfg));
+      if (max_clusters < 1) max_clusters = 1;
+      if (c->trace)
+        std::fprintf(stderr, "[rnndg] scan: hub clusters C=%d W=%d, %d co-resident\n", hc, hw,
+                     max_clusters);
+    }
+    cfg.gridDim = dim3(unsigned(max_clusters) * unsigned(hc));
+    k_sort_big<<<1, 1024, 0, c->side>>>(c->act_list.p, c->nv, c->cnt.p, c->counters.p);
+    ++c->launches;
+    RNNDG_CUDA(cudaLaunchKernelEx(&cfg, khub, a));
+  } else if (spec == 0)
     k_scan_block<kLongWarps, true><<<long_grid, 32 * kLongWarps, 0, c->side>>>(a);
   else if (long_w == 8)
     k_scan_spec<8, true, kSpec><<<long_grid, 32 * 8, 0, c->side>>>(a);
@@ -809,7 +1225,9 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     k_scan_spec<kLongWarps, true, kSpec><<<long_grid, 32 * kLongWarps, 0, c->side>>>(a);
   ++c->launches;
   RNNDG_CUDA(cudaGetLastError());
+  if (c->trace) RNNDG_CUDA(cudaEventRecord(c->ev_scan[0], c->side));
   RNNDG_LAUNCH(c, kshort, grid, threads_short, smem, a);
+  if (c->trace) RNNDG_CUDA(cudaEventRecord(c->ev_scan[1], c->stream));
   RNNDG_CUDA(cudaEventRecord(c->ev_join, c->side));
   RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
 }
