@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "librnndg.so")
+LIB_PATH = os.environ.get("RNNDG_LIB_PATH") or os.path.join(HERE, "librnndg.so")  # override: experiments only
 
 OK, EPARAM, EDATA, EINTERNAL = 0, 1, 2, 3
 X_PENDING, X_PROPOSAL, X_INEDGE, X_DELETE = 0, 1, 2, 3
