@@ -1163,6 +1163,18 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   const unsigned threads_short = 32u * unsigned(short_w);
   const size_t smem = 0;
   int per_sm = 0;
+  // shared-memory carveout in percent (RNNDG_CARVEOUT; -2 = leave the
+  // driver's choice): the scan kernels need ~51 KB (short) / 37 KB (hub) of
+  // shared memory per SM, the rest serves as L1 for the re-read rows.  C3 1M:
+  // driver default 2.18 s, 20-25% 2.15 s, 30-50% 2.16-2.18 s, 0% collapses
+  // occupancy.
+  static const int carve = [] {
+    const char* e = std::getenv("RNNDG_CARVEOUT");
+    return e ? std::atoi(e) : 25;
+  }();
+  if (carve >= -1) {
+    RNNDG_CUDA(cudaFuncSetAttribute(kshort, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
+  }
   RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kshort, threads_short, smem));
   if (c->trace && !c->scan_cfg_logged) {
     std::fprintf(stderr, "[rnndg] scan: short W=%d spec=%d ctas/SM=%d\n", short_w, spec, per_sm);
@@ -1218,6 +1230,8 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     cfg.numAttrs = 1;
     static int max_clusters = 0;
     if (!max_clusters) {
+      if (carve >= -1)
+        RNNDG_CUDA(cudaFuncSetAttribute(khub, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
       RNNDG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, khub, &cfg));
       if (max_clusters < 1) max_clusters = 1;
       if (c->trace)
