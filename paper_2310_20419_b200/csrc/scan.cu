@@ -183,6 +183,7 @@ struct ScanArgs {
   uint64_t* pend_key;
   unsigned long long* bcnt;
   unsigned long long* ctr;
+  int l2pf;  // bulk-prefetch a list's rows into L2 when its walk starts
 };
 
 __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned long long removed,
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_block(ScanArgs g) {
       const uint64_t k = L[j];
       if (!kLong) keys_sh[j] = k;
       A[j] = j;
-      prefetch_row_l2(row(k), row_bytes);
+      if (g.l2pf) prefetch_row_l2(row(k), row_bytes);
     }
     __syncthreads();
     auto rowp = [&](uint32_t, uint64_t key) -> const float* { return row(key); };
@@ -458,7 +459,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
       const uint64_t k = L[j];
       if (!kLong) keys_sh[j] = k;
       A[j] = j;
-      prefetch_row_l2(row(k), row_bytes);
+      if (g.l2pf) prefetch_row_l2(row(k), row_bytes);
     }
     __syncthreads();
     uint32_t na = U, nk = 0;
@@ -677,7 +678,7 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
   for (uint32_t i = tid; i < na; i += NT) {
     const uint32_t p = rank + i * cs;
     A[i] = p;
-    prefetch_row_l2(row(L[p]), row_bytes);
+    if (g.l2pf) prefetch_row_l2(row(L[p]), row_bytes);
   }
   if (tid == 0) sm.npk = 0;
   __syncthreads();
@@ -1141,6 +1142,13 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   a.pend_key = c->pend_key.p;
   a.bcnt = c->partitioned ? nullptr : c->bcnt.p;
   a.ctr = c->counters.p;
+  // RNNDG_L2PF=0 drops the bulk L2 prefetch of a list's rows (C3 1M: 2.15 s
+  // with it, 2.19 s without)
+  static const int l2pf = [] {
+    const char* e = std::getenv("RNNDG_L2PF");
+    return e ? std::atoi(e) : 1;
+  }();
+  a.l2pf = l2pf;
   // warps per CTA of the short-list kernel (RNNDG_SHORT_W = 2 | 4; default
   // 2: 7 CTAs of 64 threads per SM beat 4-warp CTAs, profiles/README.md)
   static const int short_w = [] {
@@ -1228,10 +1236,10 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     cfg.stream = c->side;
     cfg.attrs = &attr;
     cfg.numAttrs = 1;
+    if (carve >= -1)
+      RNNDG_CUDA(cudaFuncSetAttribute(khub, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     static int max_clusters = 0;
     if (!max_clusters) {
-      if (carve >= -1)
-        RNNDG_CUDA(cudaFuncSetAttribute(khub, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
       RNNDG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, khub, &cfg));
       if (max_clusters < 1) max_clusters = 1;
       if (c->trace)
