@@ -183,7 +183,8 @@ struct ScanArgs {
   uint64_t* pend_key;
   unsigned long long* bcnt;
   unsigned long long* ctr;
-  int l2pf;  // bulk-prefetch a list's rows into L2 when its walk starts
+  int l2pf;      // bulk-prefetch a list's rows into L2 when its walk starts
+  int coop_all;  // hubs per cluster below which every hub is walked cooperatively
 };
 
 __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned long long removed,
@@ -915,8 +916,6 @@ __device__ __forceinline__ void flush_hub(const ScanArgs& g, const HubCounters& 
   }
 }
 
-constexpr uint32_t kCoopAll = 4;  // hubs per cluster below which all are cooperative
-
 template <int W, int C, int D>
 __global__ void __launch_bounds__(32 * W, 1) k_scan_hub(ScanArgs g) {
   namespace cg = cooperative_groups;
@@ -929,7 +928,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_hub(ScanArgs g) {
   const uint32_t nmid = uint32_t(g.ctr_in[kLargeCount]);
   // few hubs in all (the tail passes): every hub is walked cooperatively,
   // the big ones (largest first, k_sort_big) before the rest
-  const bool coop_all = nbig + nmid <= kCoopAll * (gridDim.x / C);
+  const bool coop_all = nbig + nmid <= uint32_t(g.coop_all) * (gridDim.x / C);
   const uint32_t ncoop = nbig + (coop_all ? nmid : 0u);
   HubCounters hc;
   for (;;) {
@@ -1149,6 +1148,13 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return e ? std::atoi(e) : 1;
   }();
   a.l2pf = l2pf;
+  // a pass with at most RNNDG_COOP_ALL (default 4) hub lists per cluster walks
+  // every hub cooperatively (0: only the big ones)
+  static const int coop_all = [] {
+    const char* e = std::getenv("RNNDG_COOP_ALL");
+    return e ? std::atoi(e) : 4;
+  }();
+  a.coop_all = coop_all;
   // warps per CTA of the short-list kernel (RNNDG_SHORT_W = 2 | 4; default
   // 2: 7 CTAs of 64 threads per SM beat 4-warp CTAs, profiles/README.md)
   static const int short_w = [] {
