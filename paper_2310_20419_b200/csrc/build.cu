@@ -730,13 +730,10 @@ uint32_t hub_threshold() {
 // hub lists longer than this are walked by a whole thread-block cluster
 // (k_scan_hub phase 1); shorter hubs by one CTA each (RNNDG_BIG_HUB; 0 = no
 // cooperative walks)
-uint32_t big_hub_threshold() {
+uint32_t big_hub_threshold(rnndg_ctx* c) {
+  // the one-CTA-per-hub schedules have no cooperative phase
+  if (hub_cluster_size(c) == 0) return 0xFFFFFFFFu;
   static const uint32_t v = [] {
-    // the one-CTA-per-hub fallbacks (RNNDG_HUB=0, RNNDG_SPEC=0) have no
-    // cooperative phase
-    const char* h = std::getenv("RNNDG_HUB");
-    const char* sp = std::getenv("RNNDG_SPEC");
-    if ((h && std::atoi(h) == 0) || (sp && std::atoi(sp) == 0)) return 0xFFFFFFFFu;
     const char* e = std::getenv("RNNDG_BIG_HUB");
     const long x = e ? std::atol(e) : 1024;
     return x <= 0 ? 0xFFFFFFFFu : uint32_t(x < 256 ? 256 : x);
@@ -846,7 +843,7 @@ void op_scan_phase(rnndg_ctx* c) {
   if (n)
     RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
-                 big_hub_threshold());
+                 big_hub_threshold(c));
   locality_order(c);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
   launch_scan(c, c->work.p);

@@ -52,6 +52,7 @@ namespace {
 constexpr int kPushWarps = 2;    // default push scan: one 64-thread CTA per short list
 constexpr int kLongWarps = 32;   // one 1024-thread CTA per long list
 constexpr int kSpec = 4;         // provisional kept entries per push round
+constexpr size_t kNaMinRowBytes = 2048;  // rows this long stream L1::no_allocate
 
 // Chain-blocked row layout: element e < d4 = d - d % 4 lives at
 //   32 * (e / 32) + 8 * (e % 4) + (e % 32) / 4
@@ -83,12 +84,21 @@ __global__ void k_chain_layout(const float* __restrict__ x, uint64_t n, uint32_t
 // row of a pair (the candidate), L1::no_allocate so it does not evict the
 // rows that are re-read; ld256w: the row shared by many pairs (a provisional
 // kept entry), normal L1 allocation.  C3 1M: 2.25 s -> 2.18 s per build
-// (both rows no_allocate 2.20 s, w rows evict_last 2.18 s).
+// (both rows no_allocate 2.20 s, w rows evict_last 2.18 s).  Short rows
+// (C2 d = 128, C4 d = 96) stay in L1 across rounds: there the streamed row
+// is allocated too (kNA = false; C4 1M 0.97 -> 0.93 s, C2 0.79 -> 0.77 s).
+template <bool kNA = true>
 __device__ __forceinline__ void ld256(const float* p, float (&r)[8]) {
-  asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
-                 "=f"(r[6]), "=f"(r[7])
-               : "l"(p));
+  if (kNA)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                   "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
+  else
+    asm volatile("ld.global.nc.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                   "=f"(r[6]), "=f"(r[7])
+                 : "l"(p));
 }
 __device__ __forceinline__ void ld256w(const float* p, float (&r)[8]) {
   asm volatile("ld.global.nc.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
@@ -114,6 +124,7 @@ __device__ __forceinline__ void chain_step(const float (&va)[8], const float (&v
 // `a` is the streamed row, `b` the row shared across pairs (l2 is
 // bit-symmetric, so the order of the operands never changes a result).
 // Loads run two blocks ahead of the arithmetic.
+template <bool kNA = true>
 __device__ __forceinline__ float quad_l2(const float* __restrict__ a, const float* __restrict__ b,
                                          uint32_t k, uint32_t nblk, uint32_t ntail) {
   float s = 0.f;
@@ -122,23 +133,23 @@ __device__ __forceinline__ float quad_l2(const float* __restrict__ a, const floa
   float a0[8], b0[8], a1[8], b1[8];
   uint32_t blk = 0;
   if (nblk >= 2) {
-    ld256(pa, a0);
+    ld256<kNA>(pa, a0);
     ld256w(pb, b0);
-    ld256(pa + 32, a1);
+    ld256<kNA>(pa + 32, a1);
     ld256w(pb + 32, b1);
     for (blk = 2; blk + 1 < nblk; blk += 2) {
       chain_step(a0, b0, s);
-      ld256(pa + 32 * blk, a0);
+      ld256<kNA>(pa + 32 * blk, a0);
       ld256w(pb + 32 * blk, b0);
       chain_step(a1, b1, s);
-      ld256(pa + 32 * (blk + 1), a1);
+      ld256<kNA>(pa + 32 * (blk + 1), a1);
       ld256w(pb + 32 * (blk + 1), b1);
     }
     chain_step(a0, b0, s);
     chain_step(a1, b1, s);
   }
   for (; blk < nblk; ++blk) {
-    ld256(pa + 32 * blk, a0);
+    ld256<kNA>(pa + 32 * blk, a0);
     ld256w(pb + 32 * blk, b0);
     chain_step(a0, b0, s);
   }
@@ -423,7 +434,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t c, uint32_t* wcnt,
 // counting only pairs with kept entries and stopping at its first occluder --
 // the reference's exact sequence of skips and checks (builder.cpp:50-64).
 // Pairs evaluated against a w_j that turns out occluded are not counted.
-template <int W, bool kLong, int D>
+template <int W, bool kLong, int D, bool kNA = true>
 __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   constexpr uint32_t NT = 32 * W;
   constexpr uint32_t kCap = kLong ? 1 : kScanUcap;
@@ -519,7 +530,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
 #pragma unroll
           for (int i = 1; i < D; ++i)
             if (wsel == uint32_t(i)) wkey = wk[i];
-          const float dist = quad_l2(xv, row(wkey), chain, row.nblk, row.ntail);
+          const float dist = quad_l2<kNA>(xv, row(wkey), chain, row.nblk, row.ntail);
           if (has && chain == 0) tres[ti] = dist;
         }
         __syncthreads();
@@ -657,7 +668,7 @@ struct HubCounters {
 // The walk of one hub list u by `cs` cooperating CTAs (cs == C, the cluster,
 // for lists longer than big_hub_threshold(); cs == 1, this CTA alone,
 // otherwise).  rank = this CTA's rank among them.
-template <int W, int D>
+template <int W, int D, bool kNA>
 __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t cs, uint32_t rank,
                                          HubSmem<W, D>& sm, HubCounters& hc) {
   namespace cg = cooperative_groups;
@@ -792,7 +803,7 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
 #pragma unroll
         for (int i = 1; i < D; ++i)
           if (wsel == uint32_t(i)) wkey = wk[i];
-        const float dist = quad_l2(xv, row(wkey), chain, row.nblk, row.ntail);
+        const float dist = quad_l2<kNA>(xv, row(wkey), chain, row.nblk, row.ntail);
         if (has && chain == 0) sm.tres[ti] = dist;
       }
       __syncthreads();
@@ -916,7 +927,7 @@ __device__ __forceinline__ void flush_hub(const ScanArgs& g, const HubCounters& 
   }
 }
 
-template <int W, int C, int D>
+template <int W, int C, int D, bool kNA = true>
 __global__ void __launch_bounds__(32 * W, 1) k_scan_hub(ScanArgs g) {
   namespace cg = cooperative_groups;
   static_assert(C * D <= 64, "head merge holds two heads per lane");
@@ -938,7 +949,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_hub(ScanArgs g) {
     cl.sync();  // rank 0's sm.a is read before it moves on
     if (a >= ncoop) break;
     const uint32_t u = a < nbig ? g.act_list[2 * g.n - 1 - a] : g.act_list[g.n + (a - nbig)];
-    hub_walk<W, D>(g, u, C, rank, sm, hc);
+    hub_walk<W, D, kNA>(g, u, C, rank, sm, hc);
   }
   if (coop_all) return flush_hub(g, hc);
   // no DSMEM access past this point: CTAs may run (and exit) independently
@@ -948,7 +959,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_hub(ScanArgs g) {
     const uint32_t a = sm.a;
     __syncthreads();
     if (a >= nmid) break;
-    hub_walk<W, D>(g, g.act_list[g.n + a], 1, 0, sm, hc);
+    hub_walk<W, D, kNA>(g, g.act_list[g.n + a], 1, 0, sm, hc);
   }
   flush_hub(g, hc);
 }
@@ -1117,6 +1128,38 @@ void prepare_chain_layout(rnndg_ctx* c) {
   c->xp_stride = cfg.stride;
 }
 
+// provisional kept entries per push round: RNNDG_SPEC = 2 | 3 | 4 (default
+// 4, k_scan_spec) or 0 (k_scan_block, two steps per round).  At C3 1M:
+// 2 -> 2.89 s, 3 -> 2.78 s, 4 -> 2.77 s, 6 -> 3.37 s per build.
+int spec_mode() {
+  static const int v = [] {
+    const char* e = std::getenv("RNNDG_SPEC");
+    const int x = e ? std::atoi(e) : kSpec;
+    return x == 0 || x == 2 || x == 3 ? x : kSpec;
+  }();
+  return v;
+}
+
+// Hub lists on thread-block clusters of 1024-thread CTAs: returns the CTAs
+// per cluster (2 or 4), or 0 for one k_scan_spec CTA per hub.  RNNDG_HUB
+// forces 0 / 2 / 4; by default clusters of 2 for rows of >= 2 KB and one CTA
+// per hub for short rows.  C3 1M (big-hub threshold 1024): 2 -> 2.25 s,
+// 4 -> 2.26 s, 0 -> 2.42 s; clusters of 8 x 16 warps 2.38 s, 8 x 8 warps
+// 2.41 s, 4 x 4 warps 2.36 s.  C2 1M (d = 128): 0 -> 0.755 s, 2 -> 0.769 s
+// (the hub kernel's extra spills cost more than the shorter tail passes
+// save when a pair is only four blocks).
+int hub_cluster_size(rnndg_ctx* c) {
+  static const int forced = [] {
+    const char* e = std::getenv("RNNDG_HUB");
+    if (!e) return -1;
+    const int v = std::atoi(e);
+    return v == 0 || v == 4 ? v : 2;
+  }();
+  if (spec_mode() == 0) return 0;
+  if (forced >= 0) return forced;
+  return scan_config(c).stride * sizeof(float) >= kNaMinRowBytes ? 2 : 0;
+}
+
 // Launches both scan kernels; the long-list kernel runs on the side stream
 // and is joined back before returning.  work[0] / work[1] are the queues,
 // work[2] the number of short active lists.
@@ -1162,15 +1205,11 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     const int v = e ? std::atoi(e) : kPushWarps;
     return v == 2 || v == 4 ? v : kPushWarps;
   }();
-  // provisional kept entries per push round: RNNDG_SPEC = 2 | 3 | 4 (default
-  // 4, k_scan_spec) or 0 (k_scan_block, two steps per round).  At C3 1M:
-  // 2 -> 2.89 s, 3 -> 2.78 s, 4 -> 2.77 s, 6 -> 3.37 s per build.
-  static const int spec = [] {
-    const char* e = std::getenv("RNNDG_SPEC");
-    const int v = e ? std::atoi(e) : kSpec;
-    return v == 0 || v == 2 || v == 3 ? v : kSpec;
-  }();
+  const int spec = spec_mode();
+  // streamed rows L1::no_allocate only for long rows (see ld256)
+  const bool na = cfg.stride * sizeof(float) >= kNaMinRowBytes;
   auto kshort = short_w == 4 ? k_scan_spec<4, false, kSpec> : k_scan_spec<2, false, kSpec>;
+  if (!na && short_w == 2) kshort = k_scan_spec<2, false, kSpec, false>;
   if (spec == 0) kshort = short_w == 4 ? k_scan_block<4, false> : k_scan_block<2, false>;
   if (spec == 2) kshort = short_w == 4 ? k_scan_spec<4, false, 2> : k_scan_spec<2, false, 2>;
   if (spec == 3) kshort = short_w == 4 ? k_scan_spec<4, false, 3> : k_scan_spec<2, false, 3>;
@@ -1219,17 +1258,11 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return v == 8 || v == 16 ? v : kLongWarps;
   }();
   const unsigned long_grid = unsigned(sm_count(c)) * unsigned(kLongWarps / long_w) / long_div;
-  // hub lists on thread-block clusters of 1024-thread CTAs (RNNDG_HUB = CTAs
-  // per cluster: 2 (default) or 4; 0 = k_scan_spec, one CTA per hub).  C3 1M
-  // (big-hub threshold 1024): 2 -> 2.25 s, 4 -> 2.26 s, 0 -> 2.42 s; clusters
-  // of 8 x 16 warps 2.38 s, 8 x 8 warps 2.41 s, 4 x 4 warps 2.36 s.
-  static const int hub_mode = [] {
-    const char* e = std::getenv("RNNDG_HUB");
-    const int v = e ? std::atoi(e) : 2;
-    return v == 0 || v == 4 ? v : 2;
-  }();
-  if (spec != 0 && hub_mode != 0) {
+  const int hub_mode = hub_cluster_size(c);
+  if (hub_mode != 0) {
     auto khub = hub_mode == 4 ? k_scan_hub<kLongWarps, 4, kSpec> : k_scan_hub<kLongWarps, 2, kSpec>;
+    if (!na) khub = hub_mode == 4 ? k_scan_hub<kLongWarps, 4, kSpec, false>
+                                  : k_scan_hub<kLongWarps, 2, kSpec, false>;
     const int hc = hub_mode, hw = kLongWarps;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr{};
@@ -1244,10 +1277,23 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     cfg.numAttrs = 1;
     if (carve >= -1)
       RNNDG_CUDA(cudaFuncSetAttribute(khub, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
-    static int max_clusters = 0;
+    // co-resident clusters, per kernel variant (queried once each)
+    static const void* cached_fn[8] = {};
+    static int cached_clusters[8] = {};
+    int max_clusters = 0;
+    int slot = 0;
+    for (; slot < 8 && cached_fn[slot]; ++slot)
+      if (cached_fn[slot] == reinterpret_cast<const void*>(khub)) {
+        max_clusters = cached_clusters[slot];
+        break;
+      }
     if (!max_clusters) {
       RNNDG_CUDA(cudaOccupancyMaxActiveClusters(&max_clusters, khub, &cfg));
       if (max_clusters < 1) max_clusters = 1;
+      if (slot < 8) {
+        cached_fn[slot] = reinterpret_cast<const void*>(khub);
+        cached_clusters[slot] = max_clusters;
+      }
       if (c->trace)
         std::fprintf(stderr, "[rnndg] scan: hub clusters C=%d W=%d, %d co-resident\n", hc, hw,
                      max_clusters);

@@ -23,6 +23,10 @@ struct ScanConfig {
 ScanConfig scan_config(rnndg_ctx* c);
 void prepare_chain_layout(rnndg_ctx* c);
 void launch_scan(rnndg_ctx* c, unsigned int* work);
+// provisional entries per push round (RNNDG_SPEC) and the hub-cluster size
+// (0 = one CTA per hub list); build.cu queues big hubs only when clustered
+int spec_mode();
+int hub_cluster_size(rnndg_ctx* c);
 // cached distances of the random initial lists (k_random_init left the raw
 // samples in the keys' low 32 bits)
 void launch_init_dists(rnndg_ctx* c, uint32_t S);
