@@ -824,6 +824,7 @@ void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
   c->has_graph = true;
   c->has_distances = true;
   c->exact_dists = true;
+  c->bulk_fresh = true;
   op_sort_lists(c);  // establish the sorted-list invariant
 }
 
@@ -881,6 +882,7 @@ void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t
   if (t_scan) *t_scan += elapsed_ms(c->ev[1], c->ev[2]) * 1e-3;
   if (t_apply) *t_apply += elapsed_ms(c->ev[2], c->ev[3]) * 1e-3;
   if (touched) *touched += h[kTouched];
+  c->hubs_prev = h[kLargeCount] + h[kBigCount];
   if (active_entries) *active_entries += h[kActiveEntries];
   if (c->trace)
     std::fprintf(stderr,
@@ -974,6 +976,7 @@ void in_prune(rnndg_ctx* c, uint32_t R) {
 void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
   if (R < 1) throw ParamError("add_reverse_edges: R must be >= 1");
   if (!c->has_distances) throw ParamError("add_reverse_edges: graph has no distances");
+  c->bulk_fresh = true;
   const uint64_t n = c->nv;
   ensure_scratch(c);
   // 1. reversals bucketed by their source (= target of the forward edge)

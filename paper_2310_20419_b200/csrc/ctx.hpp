@@ -156,6 +156,11 @@ struct rnndg_ctx {
   std::vector<rnndg_counts> pass_counts;
   bool trace = false;  // RNNDG_TRACE=1: per-pass line on stderr
   bool scan_cfg_logged = false;
+  // hub lists in the previous update pass (~0: unknown) and whether the lists
+  // were rebuilt in bulk since (random init, reverse phase, imported graph):
+  // picks the hub-cluster size of the next scan
+  uint64_t hubs_prev = ~0ull;
+  bool bulk_fresh = true;
   // shard scans since the last rnndg_shard_totals(reset): distance-stage time
   // and the SURVEY 8(d) units, for the sharded bench roofline
   double shard_scan_s = 0.0;

@@ -53,6 +53,8 @@ constexpr int kPushWarps = 2;    // default push scan: one 64-thread CTA per sho
 constexpr int kLongWarps = 32;   // one 1024-thread CTA per long list
 constexpr int kSpec = 4;         // provisional kept entries per push round
 constexpr size_t kNaMinRowBytes = 2048;  // rows this long stream L1::no_allocate
+constexpr uint64_t kTail4Hubs = 600;     // hub lists per pass for clusters of 4
+constexpr uint64_t kTail8Hubs = 64;      // ... and of 8
 
 // Chain-blocked row layout: element e < d4 = d - d % 4 lives at
 //   32 * (e / 32) + 8 * (e % 4) + (e % 32) / 4
@@ -1160,6 +1162,22 @@ int hub_cluster_size(rnndg_ctx* c) {
   return scan_config(c).stride * sizeof(float) >= kNaMinRowBytes ? 2 : 0;
 }
 
+// Cluster size for this pass's hub kernel, when clusters are on (default
+// schedule): pairs while hub lists are many, larger clusters for the tail
+// passes whose few hubs set the critical path.  The hub count only falls
+// between bulk rebuilds, so the previous pass's count bounds this one's.
+// RNNDG_HUB_TAIL=0 keeps pairs throughout.
+int hub_cluster_for_pass(rnndg_ctx* c, int mode) {
+  static const int tail = [] {
+    const char* e = std::getenv("RNNDG_HUB_TAIL");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (mode != 2 || !tail || c->bulk_fresh) return mode;
+  if (c->hubs_prev <= kTail8Hubs) return 8;
+  if (c->hubs_prev <= kTail4Hubs) return 4;
+  return 2;
+}
+
 // Launches both scan kernels; the long-list kernel runs on the side stream
 // and is joined back before returning.  work[0] / work[1] are the queues,
 // work[2] the number of short active lists.
@@ -1258,12 +1276,15 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return v == 8 || v == 16 ? v : kLongWarps;
   }();
   const unsigned long_grid = unsigned(sm_count(c)) * unsigned(kLongWarps / long_w) / long_div;
-  const int hub_mode = hub_cluster_size(c);
+  const int hub_mode = hub_cluster_for_pass(c, hub_cluster_size(c));
+  c->bulk_fresh = false;
   if (hub_mode != 0) {
-    auto khub = hub_mode == 4 ? k_scan_hub<kLongWarps, 4, kSpec> : k_scan_hub<kLongWarps, 2, kSpec>;
+    auto khub = k_scan_hub<kLongWarps, 2, kSpec>;
+    if (hub_mode == 4) khub = k_scan_hub<kLongWarps, 4, kSpec>;
+    if (hub_mode == 8) khub = k_scan_hub<kLongWarps, 8, kSpec>;
     if (!na) khub = hub_mode == 4 ? k_scan_hub<kLongWarps, 4, kSpec, false>
                                   : k_scan_hub<kLongWarps, 2, kSpec, false>;
-    const int hc = hub_mode, hw = kLongWarps;
+    const int hc = !na && hub_mode == 8 ? 2 : hub_mode, hw = kLongWarps;
     cudaLaunchConfig_t cfg{};
     cudaLaunchAttribute attr{};
     attr.id = cudaLaunchAttributeClusterDimension;
