@@ -53,8 +53,8 @@ constexpr int kPushWarps = 2;    // default push scan: one 64-thread CTA per sho
 constexpr int kLongWarps = 32;   // one 1024-thread CTA per long list
 constexpr int kSpec = 4;         // provisional kept entries per push round
 constexpr size_t kNaMinRowBytes = 2048;  // rows this long stream L1::no_allocate
-constexpr uint64_t kTail4Hubs = 600;     // hub lists per pass for clusters of 4
-constexpr uint64_t kTail8Hubs = 64;      // ... and of 8
+constexpr uint64_t kTail4Hubs = 3000;    // hub lists per pass for clusters of 4
+constexpr uint64_t kTail8Hubs = 400;     // ... and of 8
 
 // Chain-blocked row layout: element e < d4 = d - d % 4 lives at
 //   32 * (e / 32) + 8 * (e % 4) + (e % 32) / 4
@@ -1166,7 +1166,9 @@ int hub_cluster_size(rnndg_ctx* c) {
 // schedule): pairs while hub lists are many, larger clusters for the tail
 // passes whose few hubs set the critical path.  The hub count only falls
 // between bulk rebuilds, so the previous pass's count bounds this one's.
-// RNNDG_HUB_TAIL=0 keeps pairs throughout.
+// RNNDG_HUB_TAIL=0 keeps pairs throughout.  C3 1M: pairs throughout 2.149 s;
+// clusters of 4 / 8 up to 600 / 64 hubs 2.137 s, 1500 / 200 2.128 s,
+// 3000 / 400 2.125 s, 6000 / 800 2.126 s, 10000 / 1500 2.147 s.
 int hub_cluster_for_pass(rnndg_ctx* c, int mode) {
   static const int tail = [] {
     const char* e = std::getenv("RNNDG_HUB_TAIL");
