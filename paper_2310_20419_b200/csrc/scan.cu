@@ -198,6 +198,7 @@ struct ScanArgs {
   unsigned long long* ctr;
   int l2pf;      // bulk-prefetch a list's rows into L2 when its walk starts
   int coop_all;  // hubs per cluster below which every hub is walked cooperatively
+  int run_max;   // longest leading run of old entries kept in one round (0: off)
 };
 
 __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned long long removed,
@@ -450,6 +451,9 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   __shared__ uint32_t s_a, s_kept;
   __shared__ uint32_t s_tb[D];     // task base of candidates 1 .. D-1
   __shared__ uint32_t s_nm[D];     // their need masks
+  __shared__ uint32_t s_run;       // old-run rounds: window length,
+  __shared__ uint32_t s_rp[32];    //   its list positions
+  __shared__ uint64_t s_rk[32];    //   and keys
   const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
   const uint32_t quad = lane >> 2, chain = lane & 3;
   const Row row = g.row;
@@ -478,6 +482,97 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
     __syncthreads();
     uint32_t na = U, nk = 0;
     while (na) {
+      if (g.run_max) {
+        // Old-run round.  The alive entries ahead of the first fresh one are
+        // all old: each was tested against every earlier kept entry already,
+        // and old/old pairs are skipped (builder.cpp:53-56), so the whole
+        // run is kept at once -- no provisional fates to resolve -- and only
+        // the fresh candidates after it need distances, one per run entry.
+        // Used when the run is longer than D and its tasks fit the task
+        // arrays; otherwise the speculative round below.
+        uint32_t fr = 0;
+        for (uint32_t j = tid; j < na; j += NT) fr += key_fresh(K[A[j]]) ? 1u : 0u;
+        uint32_t ftot;
+        block_excl_scan<W>(fr, wcnt, ftot);
+        if (wid == 0) {
+          const bool old = lane < na && !key_fresh(K[A[lane]]);
+          const unsigned m = ~__ballot_sync(0xffffffffu, old);
+          uint32_t run = m ? uint32_t(__ffs(m)) - 1u : 32u;
+          if (run > uint32_t(g.run_max)) run = uint32_t(g.run_max);
+          const uint32_t fb = ftot < NT ? ftot : NT;  // fresh candidates per batch, at most
+          const uint32_t cap = kTasks / (fb ? fb : 1u);
+          if (run > cap) run = cap;
+          if (lane < run) {
+            s_rp[lane] = A[lane];
+            s_rk[lane] = K[A[lane]];
+          }
+          if (lane == 0) s_run = run;
+        }
+        __syncthreads();
+        const uint32_t wr = s_run;
+        if (wr > uint32_t(D)) {
+          if (tid == 0) skips += uint64_t(wr) * (wr - 1) / 2;  // run entries among themselves
+          uint32_t nn = 0;
+          for (uint32_t b0 = wr; b0 < na; b0 += NT) {
+            const uint32_t ai = b0 + tid;
+            const bool valid = ai < na;
+            const uint32_t q = valid ? A[ai] : 0u;
+            const uint64_t vk = valid ? K[q] : 0ull;
+            const bool vf = valid && key_fresh(vk);
+            uint32_t ntask;
+            const uint32_t tb = block_excl_scan<W>(vf ? wr : 0u, wcnt, ntask);
+            evals += tid == 0 ? ntask : 0u;
+            if (vf)
+              for (uint32_t i = 0; i < wr; ++i) {
+                tq[tb + i] = q;
+                tw[tb + i] = uint8_t(i);
+              }
+            if (valid && !vf) skips += wr;
+            __syncthreads();
+            for (uint32_t t0 = 0; t0 < ntask; t0 += 8 * W) {
+              const uint32_t twp = t0 + 8 * wid;
+              if (twp >= ntask) continue;  // warp-uniform
+              const uint32_t ti = twp + quad;
+              const bool has = ti < ntask;
+              const uint32_t ts = has ? ti : twp;
+              const float dist = quad_l2<kNA>(row(K[tq[ts]]), row(s_rk[tw[ts]]), chain, row.nblk,
+                                              row.ntail);
+              if (has && chain == 0) tres[ti] = dist;
+            }
+            __syncthreads();
+            bool gone = false;
+            if (vf) {
+              for (uint32_t i = 0; i < wr; ++i) {
+                const float d = tres[tb + i];
+                ++checks;
+                T[q] = 1;
+                T[s_rp[i]] = 1;
+                if (key_dist(vk) >= d) {
+                  gone = true;
+                  ++removed;
+                  const uint32_t w_id = key_id(s_rk[i]);
+                  g.pend_src[base + q] = w_id;
+                  g.pend_key[base + q] = make_key(d, key_id(vk), 1u);
+                  if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
+                  break;
+                }
+              }
+            }
+            const bool stay = valid && !gone;
+            uint32_t nstay;
+            const uint32_t r = block_rank<W>(stay, wcnt, nstay);
+            if (stay) A[nn + r] = q;
+            nn += nstay;
+            __syncthreads();
+          }
+          if (tid == 0)
+            for (uint32_t i = 0; i < wr; ++i) L[nk + i] = s_rk[i];  // old already
+          nk += wr;
+          na = nn;
+          __syncthreads();
+          continue;
+        }
+      }
       const uint32_t De = na < uint32_t(D) ? na : uint32_t(D);
       uint64_t wk[D];
       uint32_t wp[D];
@@ -1218,6 +1313,14 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return e ? std::atoi(e) : 4;
   }();
   a.coop_all = coop_all;
+  // old-run rounds (RNNDG_RUN = longest run kept per round, <= 32; 0 = off).
+  // C3 1M: off 2.141 s, 16 2.115 s, 32 2.123 s
+  static const int run_max = [] {
+    const char* e = std::getenv("RNNDG_RUN");
+    const int v = e ? std::atoi(e) : 16;
+    return v < 0 ? 0 : (v > 32 ? 32 : v);
+  }();
+  a.run_max = run_max;
   // warps per CTA of the short-list kernel (RNNDG_SHORT_W = 2 | 4; default
   // 2: 7 CTAs of 64 threads per SM beat 4-warp CTAs, profiles/README.md)
   static const int short_w = [] {
