@@ -750,12 +750,13 @@ struct HubSmem {
   uint8_t tw[kTasks];
   float tres[kTasks];
   uint32_t wcnt[W];
-  uint32_t head[2][D];
-  uint32_t na[2];
-  uint32_t a, tot, kept, npk;
-  uint32_t wp[D];
+  uint32_t head[2][32];   // first alive positions, pos << 1 | fresh
+  uint32_t na[2], nfr[2]; // alive and fresh-alive counts
+  uint32_t a, tot, kept, npk, run;
+  uint32_t wp[32];        // the merged first positions (pos << 1 | fresh)
   uint32_t tb[D], nm[D];  // fate tasks of w_2 .. w_D
-  uint64_t pk[D];         // kept keys of the previous round (rank 0)
+  uint64_t rk[32];        // old-run window keys
+  uint64_t pk[32];        // kept keys of the previous round (rank 0)
 };
 
 struct HubCounters {
@@ -791,11 +792,29 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
   }
   if (tid == 0) sm.npk = 0;
   __syncthreads();
+  // heads published per CTA: the first H alive positions of every CTA hold
+  // the first H of the whole list (old-run windows are at most H long)
+  const uint32_t H = 64 / (cs < 2 ? 2u : cs) < 32u ? 64 / (cs < 2 ? 2u : cs) : 32u;
   uint32_t nk = 0, ao = 0;
   for (uint32_t rnd = 0;; ++rnd) {
     const uint32_t buf = rnd & 1u;
-    if (tid < uint32_t(D)) sm.head[buf][tid] = tid < na ? A[ao + tid] : kInf;
-    if (tid == 0) sm.na[buf] = na;
+    uint32_t fr = 0;  // fresh alive entries of this CTA
+    if (g.run_max)
+      for (uint32_t j = tid; j < na; j += NT) fr += key_fresh(L[A[ao + j]]) ? 1u : 0u;
+    uint32_t nfr;
+    block_excl_scan<W>(fr, sm.wcnt, nfr);
+    if (tid < H) {
+      uint32_t h = kInf;
+      if (tid < na) {
+        const uint32_t p = A[ao + tid];
+        h = p << 1 | key_fresh(L[p]);
+      }
+      sm.head[buf][tid] = h;
+    }
+    if (tid == 0) {
+      sm.na[buf] = na;
+      sm.nfr[buf] = nfr;
+    }
     if (coop)
       cl.sync();
     else
@@ -803,37 +822,129 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
     if (rank == 0 && tid == 0)
       for (uint32_t i = 0; i < sm.npk; ++i) L[nk - sm.npk + i] = sm.pk[i];
     if (wid == 0) {
-      // D smallest of the cs*D published heads, and the total alive count
-      uint32_t h0 = kInf, h1 = kInf, cnt = 0;
+      // the H smallest of the cs*H published heads in order, the total alive
+      // and fresh-alive counts, and the old run at the head of the list
+      uint32_t h0 = kInf, h1 = kInf, cnt = 0, fcnt = 0;
       if (coop) {
-        if (lane < cs * D) h0 = cl.map_shared_rank(&sm.head[buf][0], lane / D)[lane % D];
-        if (lane + 32 < cs * D)
-          h1 = cl.map_shared_rank(&sm.head[buf][0], (lane + 32) / D)[(lane + 32) % D];
-        if (lane < cs) cnt = *cl.map_shared_rank(&sm.na[buf], lane);
+        if (lane < cs * H) h0 = cl.map_shared_rank(&sm.head[buf][0], lane / H)[lane % H];
+        if (lane + 32 < cs * H)
+          h1 = cl.map_shared_rank(&sm.head[buf][0], (lane + 32) / H)[(lane + 32) % H];
+        if (lane < cs) {
+          cnt = *cl.map_shared_rank(&sm.na[buf], lane);
+          fcnt = *cl.map_shared_rank(&sm.nfr[buf], lane);
+        }
       } else {
-        if (lane < uint32_t(D)) h0 = sm.head[buf][lane];
-        if (lane == 0) cnt = sm.na[buf];
+        if (lane < H) h0 = sm.head[buf][lane];
+        if (lane == 0) {
+          cnt = sm.na[buf];
+          fcnt = sm.nfr[buf];
+        }
       }
       const uint32_t tot = __reduce_add_sync(0xffffffffu, cnt);
-#pragma unroll
-      for (int i = 0; i < D; ++i) {
+      const uint32_t ftot = __reduce_add_sync(0xffffffffu, fcnt);
+      uint32_t run = 0;
+      bool in_run = g.run_max != 0;
+      for (uint32_t i = 0; i < H; ++i) {
         const uint32_t m = __reduce_min_sync(0xffffffffu, h0 < h1 ? h0 : h1);
         if (h0 == m) h0 = kInf;
         if (h1 == m) h1 = kInf;
         if (lane == 0) sm.wp[i] = m;
+        in_run = in_run && m != kInf && !(m & 1u);
+        run += in_run ? 1u : 0u;
+        if (i + 1 >= uint32_t(D) && !in_run) break;  // warp-uniform
       }
-      if (lane == 0) sm.tot = tot;
+      if (run > uint32_t(g.run_max)) run = uint32_t(g.run_max);
+      const uint32_t fb = ftot < NT ? ftot : NT;  // fresh candidates per CTA batch, at most
+      const uint32_t cap = (NT * D) / (fb ? fb : 1u);
+      if (run > cap) run = cap;
+      if (lane == 0) {
+        sm.tot = tot;
+        sm.run = run;
+      }
     }
     __syncthreads();
     const uint32_t tot = sm.tot;
     if (tot == 0) break;
+    const uint32_t wr = sm.run;
+    if (wr > uint32_t(D)) {
+      // Old-run round (k_scan_spec's): the run is kept whole, only fresh
+      // candidates are tested against it; the owner pops its run entries.
+      uint32_t own = 0;
+      for (uint32_t i = 0; i < wr; ++i) own += (sm.wp[i] >> 1) % cs == rank ? 1u : 0u;
+      if (tid < wr) sm.rk[tid] = L[sm.wp[tid] >> 1];
+      if (rank == 0 && tid == 0) hc.skips += uint64_t(wr) * (wr - 1) / 2;
+      ao += own;
+      na -= own;
+      __syncthreads();
+      uint32_t nn = 0;
+      for (uint32_t b0 = 0; b0 < na; b0 += NT) {
+        const uint32_t ai = b0 + tid;
+        const bool valid = ai < na;
+        const uint32_t q = valid ? A[ao + ai] : 0u;
+        const uint64_t vk = valid ? L[q] : 0ull;
+        const bool vf = valid && key_fresh(vk);
+        uint32_t ntask;
+        const uint32_t tb = block_excl_scan<W>(vf ? wr : 0u, sm.wcnt, ntask);
+        hc.evals += tid == 0 ? ntask : 0u;
+        if (vf)
+          for (uint32_t i = 0; i < wr; ++i) {
+            sm.tq[tb + i] = q;
+            sm.tw[tb + i] = uint8_t(i);
+          }
+        if (valid && !vf) hc.skips += wr;
+        __syncthreads();
+        for (uint32_t t0 = 0; t0 < ntask; t0 += 8 * W) {
+          const uint32_t twp = t0 + 8 * wid;
+          if (twp >= ntask) continue;  // warp-uniform
+          const uint32_t ti = twp + quad;
+          const bool has = ti < ntask;
+          const uint32_t ts = has ? ti : twp;
+          const float dist = quad_l2<kNA>(row(L[sm.tq[ts]]), row(sm.rk[sm.tw[ts]]), chain,
+                                          row.nblk, row.ntail);
+          if (has && chain == 0) sm.tres[ti] = dist;
+        }
+        __syncthreads();
+        bool gone = false;
+        if (vf) {
+          for (uint32_t i = 0; i < wr; ++i) {
+            const float d = sm.tres[tb + i];
+            ++hc.checks;
+            T[q] = 1;
+            T[sm.wp[i] >> 1] = 1;
+            if (key_dist(vk) >= d) {
+              gone = true;
+              ++hc.removed;
+              const uint32_t w_id = key_id(sm.rk[i]);
+              g.pend_src[base + q] = w_id;
+              g.pend_key[base + q] = make_key(d, key_id(vk), 1u);
+              if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
+              break;
+            }
+          }
+        }
+        const bool stay = valid && !gone;
+        uint32_t nstay;
+        const uint32_t r = block_rank<W>(stay, sm.wcnt, nstay);
+        if (stay) A[nn + r] = q;
+        nn += nstay;
+        __syncthreads();
+      }
+      if (rank == 0 && tid == 0) {
+        for (uint32_t i = 0; i < wr; ++i) sm.pk[i] = sm.rk[i];  // old already
+        sm.npk = wr;
+      }
+      nk += wr;
+      na = nn;
+      ao = 0;
+      continue;
+    }
     const uint32_t De = tot < uint32_t(D) ? tot : uint32_t(D);
     uint64_t wk[D];
     uint32_t wp[D];
     uint32_t own = 0;  // w's owned by this CTA: its first `own` alive entries
 #pragma unroll
     for (int i = 0; i < D; ++i) {
-      wp[i] = uint32_t(i) < De ? sm.wp[i] : sm.wp[0];
+      wp[i] = (uint32_t(i) < De ? sm.wp[i] : sm.wp[0]) >> 1;
       wk[i] = L[wp[i]];
       own += (uint32_t(i) < De && wp[i] % cs == rank) ? 1u : 0u;
     }
