@@ -199,6 +199,7 @@ struct ScanArgs {
   int l2pf;      // bulk-prefetch a list's rows into L2 when its walk starts
   int coop_all;  // hubs per cluster below which every hub is walked cooperatively
   int run_max;   // longest leading run of old entries kept in one round (0: off)
+  int run_tasks; // task budget of an old-run round per 64 threads
 };
 
 __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned long long removed,
@@ -500,7 +501,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
           uint32_t run = m ? uint32_t(__ffs(m)) - 1u : 32u;
           if (run > uint32_t(g.run_max)) run = uint32_t(g.run_max);
           const uint32_t fb = ftot < NT ? ftot : NT;  // fresh candidates per batch, at most
-          const uint32_t cap = kTasks / (fb ? fb : 1u);
+          const uint32_t budget = min(kTasks, uint32_t(g.run_tasks) * (NT / 64));
+          const uint32_t cap = budget / (fb ? fb : 1u);
           if (run > cap) run = cap;
           if (lane < run) {
             s_rp[lane] = A[lane];
@@ -855,7 +857,7 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
       }
       if (run > uint32_t(g.run_max)) run = uint32_t(g.run_max);
       const uint32_t fb = ftot < NT ? ftot : NT;  // fresh candidates per CTA batch, at most
-      const uint32_t cap = (NT * D) / (fb ? fb : 1u);
+      const uint32_t cap = min(NT * D, uint32_t(g.run_tasks) * (NT / 64)) / (fb ? fb : 1u);
       if (run > cap) run = cap;
       if (lane == 0) {
         sm.tot = tot;
@@ -1432,6 +1434,12 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return v < 0 ? 0 : (v > 32 ? 32 : v);
   }();
   a.run_max = run_max;
+  static const int run_tasks = [] {
+    const char* e = std::getenv("RNNDG_RUN_TASKS");
+    const int v = e ? std::atoi(e) : 256;
+    return v < 1 ? 1 : v;
+  }();
+  a.run_tasks = run_tasks;
   // warps per CTA of the short-list kernel (RNNDG_SHORT_W = 2 | 4; default
   // 2: 7 CTAs of 64 threads per SM beat 4-warp CTAs, profiles/README.md)
   static const int short_w = [] {
