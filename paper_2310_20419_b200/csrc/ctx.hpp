@@ -118,6 +118,7 @@ struct rnndg_ctx {
   rnndg::DevBuf<uint64_t> okey, act_small;
   rnndg::DevBuf<uint32_t> act_list, pend_src, bpay, bpay_s;
   rnndg::DevBuf<uint64_t> pend_key, bkey, bkey_s, seg_end, boff;
+  rnndg::DevBuf<uint32_t> seg_big;  // segmented sort: count + segments longer than a warp sorts
   rnndg::DevBuf<unsigned long long> bcnt, bcur;
   rnndg::DevBuf<uint32_t> post_cnt;
   rnndg::DevBuf<unsigned long long> counters;
