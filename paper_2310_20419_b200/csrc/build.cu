@@ -30,6 +30,7 @@
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
+#include <cub/iterator/counting_input_iterator.cuh>
 #include <cub/iterator/transform_input_iterator.cuh>
 
 #include <algorithm>
@@ -117,58 +118,58 @@ __global__ void k_fill_offsets(uint64_t n, uint32_t S, uint64_t* off, uint32_t* 
 }
 
 // ------------------------------------------------------------ mark active
-// Long lists (> kScanUcap) are queued to act_list[n ..) for the CTA scan;
-// short active lists are selected later in locality order.
-__global__ void k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
-                              const uint32_t* __restrict__ cnt,
-                              const uint64_t* __restrict__ key,
-                              uint8_t* __restrict__ active,
-                              uint32_t* __restrict__ act_list,
-                              uint32_t* __restrict__ post_cnt,
-                              unsigned long long* __restrict__ ctr, uint32_t ucap,
-                              uint32_t big_cap) {
-  const uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x;
-  unsigned long long skips = 0, aentries = 0, nact = 0;
-  bool large = false, big = false;
-  if (u < n) {
+// active = the list holds a fresh entry (builder.cpp:53-56: otherwise every
+// pair is old/old and the scan only counts skips).  One warp per list
+// (coalesced key reads, ballot), persistent warps; counters reduced per warp
+// and added once per warp at the end.  Lists longer than ucap go to the hub
+// queues: act_list[n + i] (<= big_cap) and act_list[2n - 1 - i] (> big_cap);
+// short active lists are selected later (locality_order).
+__global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t* __restrict__ off,
+                                                    const uint32_t* __restrict__ cnt,
+                                                    const uint64_t* __restrict__ key,
+                                                    uint8_t* __restrict__ active,
+                                                    uint32_t* __restrict__ act_list,
+                                                    uint32_t* __restrict__ post_cnt,
+                                                    unsigned long long* __restrict__ ctr,
+                                                    uint32_t ucap, uint32_t big_cap) {
+  const uint32_t lane = lane_id();
+  const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long skips = 0, aentries = 0, nact = 0, maxlen = 0;
+  for (uint64_t u = warp; u < n; u += nwarps) {
     const uint64_t b = off[u];
     const uint32_t U = cnt[u];
     bool act = false;
-    for (uint32_t j = 0; j < U; ++j)
-      if (key_fresh(key[b + j])) {
-        act = true;
-        break;
-      }
+    for (uint32_t j0 = 0; j0 < U && !act; j0 += 32) {
+      const uint32_t j = j0 + lane;
+      act = __any_sync(0xffffffffu, j < U && key_fresh(key[b + j]));
+    }
+    if (lane != 0) continue;
     uint8_t flag = 0;
     if (act) {
-      aentries = U;
-      nact = 1;
-      big = U > big_cap;
-      large = U > ucap && !big;
+      aentries += U;
+      nact += 1;
+      maxlen = U > maxlen ? U : maxlen;
       flag = U > ucap ? 2 : 1;
-      atomicMax(&ctr[kMaxLen], (unsigned long long)U);
+      if (U > big_cap) {
+        const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kBigCount]), 1u);
+        act_list[2 * n - 1 - x] = uint32_t(u);
+      } else if (U > ucap) {
+        const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLargeCount]), 1u);
+        act_list[n + x] = uint32_t(u);
+      }
     } else {
       post_cnt[u] = U;
-      skips = (unsigned long long)U * (U ? U - 1 : 0) / 2;
+      skips += (unsigned long long)U * (U ? U - 1 : 0) / 2;
     }
     active[u] = flag;
   }
-  const unsigned ml = __ballot_sync(0xffffffffu, large);
-  uint32_t bl = 0;
-  if (lane_id() == 0 && ml)
-    bl = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLargeCount]), __popc(ml));
-  bl = __shfl_sync(0xffffffffu, bl, 0);
-  if (large) act_list[n + bl + __popc(ml & ((1u << lane_id()) - 1))] = uint32_t(u);
-  // lists longer than big_cap are queued from the end, act_list[2n - 1 - i]
-  const unsigned mb = __ballot_sync(0xffffffffu, big);
-  uint32_t bb = 0;
-  if (lane_id() == 0 && mb)
-    bb = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kBigCount]), __popc(mb));
-  bb = __shfl_sync(0xffffffffu, bb, 0);
-  if (big) act_list[2 * n - 1 - (bb + __popc(mb & ((1u << lane_id()) - 1)))] = uint32_t(u);
-  warp_add_counter(&ctr[kFlagSkips], skips);
-  warp_add_counter(&ctr[kActiveEntries], aentries);
-  warp_add_counter(&ctr[kActiveCount], nact);
+  if (lane == 0) {
+    if (skips) atomicAdd(&ctr[kFlagSkips], skips);
+    if (aentries) atomicAdd(&ctr[kActiveEntries], aentries);
+    if (nact) atomicAdd(&ctr[kActiveCount], nact);
+    if (maxlen) atomicMax(&ctr[kMaxLen], maxlen);
+  }
 }
 
 // ---------------------------------------------------------- locality order
@@ -891,9 +892,15 @@ void locality_order(rnndg_ctx* c) {
   uint64_t* ok2 = c->okey.p + n;
   size_t bytes = 0;
   if (mode == 0) {
-    RNNDG_LAUNCH(c, k_label_step, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
-                 nullptr, la, 1);
-    RNNDG_LAUNCH(c, k_order_keys, grid_for(n, 256), 256, 0, n, la, ok2);  // already sorted
+    // vertex index order: select straight from the index sequence
+    int* nsel0 = reinterpret_cast<int*>(c->work.p + 2);
+    cub::CountingInputIterator<uint64_t> idx(0);
+    RNNDG_CUDA(cub::DeviceSelect::If(nullptr, bytes, idx, c->act_small.p, nsel0, int64_t(n),
+                                     IsShortActive{c->active.p}, c->stream));
+    RNNDG_CUDA(cub::DeviceSelect::If(cub_temp(c, bytes), bytes, idx, c->act_small.p, nsel0,
+                                     int64_t(n), IsShortActive{c->active.p}, c->stream));
+    c->launches += 2;
+    return;
   } else {
     if (mode == 2) {
       RNNDG_LAUNCH(c, k_len_keys, grid_for(n, 256), 256, 0, n, c->cnt.p, ok);
@@ -971,7 +978,7 @@ void op_scan_phase(rnndg_ctx* c) {
   zero(c, c->bcur.p, n);
   RNNDG_CUDA(cudaEventRecord(c->ev[0], c->stream));
   if (n)
-    RNNDG_LAUNCH(c, k_mark_active, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, c->key.p,
+    RNNDG_LAUNCH(c, k_mark_active, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
                  big_hub_threshold(c));
   locality_order(c);
