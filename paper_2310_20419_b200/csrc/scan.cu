@@ -51,7 +51,8 @@ namespace {
 
 constexpr int kPushWarps = 2;    // default push scan: one 64-thread CTA per short list
 constexpr int kLongWarps = 32;   // one 1024-thread CTA per long list
-constexpr int kSpec = 4;         // provisional kept entries per push round
+constexpr int kSpec = 4;         // provisional kept entries per push round (hub lists)
+constexpr int kShortSpec = 3;    // ... and for short lists (RNNDG_SPEC)
 constexpr size_t kNaMinRowBytes = 2048;  // rows this long stream L1::no_allocate
 constexpr uint64_t kTail4Hubs = 3000;    // hub lists per pass for clusters of 4
 constexpr uint64_t kTail8Hubs = 400;     // ... and of 8
@@ -1338,14 +1339,16 @@ void prepare_chain_layout(rnndg_ctx* c) {
   c->xp_stride = cfg.stride;
 }
 
-// provisional kept entries per push round: RNNDG_SPEC = 2 | 3 | 4 (default
-// 4, k_scan_spec) or 0 (k_scan_block, two steps per round).  At C3 1M:
-// 2 -> 2.89 s, 3 -> 2.78 s, 4 -> 2.77 s, 6 -> 3.37 s per build.
+// provisional kept entries per push round of the short-list kernel:
+// RNNDG_SPEC = 2 | 3 | 4 (default 3) or 0 (k_scan_block, two steps per round,
+// one CTA per hub).  C3 1M before old-run rounds: 2 -> 2.89 s, 3 -> 2.78 s,
+// 4 -> 2.77 s, 6 -> 3.37 s; with them: 2 -> 2.048 s, 3 -> 2.026 s, 4 ->
+// 2.051 s (hub walks keep 4: 3 there costs 2.045 s).
 int spec_mode() {
   static const int v = [] {
     const char* e = std::getenv("RNNDG_SPEC");
-    const int x = e ? std::atoi(e) : kSpec;
-    return x == 0 || x == 2 || x == 3 ? x : kSpec;
+    const int x = e ? std::atoi(e) : kShortSpec;
+    return x == 0 || x == 2 || x == 3 || x == 4 ? x : kShortSpec;
   }();
   return v;
 }
@@ -1440,21 +1443,18 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return v < 1 ? 1 : v;
   }();
   a.run_tasks = run_tasks;
-  // warps per CTA of the short-list kernel (RNNDG_SHORT_W = 2 | 4; default
-  // 2: 7 CTAs of 64 threads per SM beat 4-warp CTAs, profiles/README.md)
-  static const int short_w = [] {
-    const char* e = std::getenv("RNNDG_SHORT_W");
-    const int v = e ? std::atoi(e) : kPushWarps;
-    return v == 2 || v == 4 ? v : kPushWarps;
-  }();
+  // two-warp CTAs for short lists (4-warp CTAs measured slower,
+  // profiles/README.md)
+  constexpr int short_w = kPushWarps;
   const int spec = spec_mode();
   // streamed rows L1::no_allocate only for long rows (see ld256)
   const bool na = cfg.stride * sizeof(float) >= kNaMinRowBytes;
-  auto kshort = short_w == 4 ? k_scan_spec<4, false, kSpec> : k_scan_spec<2, false, kSpec>;
-  if (!na && short_w == 2) kshort = k_scan_spec<2, false, kSpec, false>;
-  if (spec == 0) kshort = short_w == 4 ? k_scan_block<4, false> : k_scan_block<2, false>;
-  if (spec == 2) kshort = short_w == 4 ? k_scan_spec<4, false, 2> : k_scan_spec<2, false, 2>;
-  if (spec == 3) kshort = short_w == 4 ? k_scan_spec<4, false, 3> : k_scan_spec<2, false, 3>;
+  auto kshort = na ? k_scan_spec<short_w, false, 3, true> : k_scan_spec<short_w, false, 3, false>;
+  if (spec == 4)
+    kshort = na ? k_scan_spec<short_w, false, 4, true> : k_scan_spec<short_w, false, 4, false>;
+  if (spec == 2)
+    kshort = na ? k_scan_spec<short_w, false, 2, true> : k_scan_spec<short_w, false, 2, false>;
+  if (spec == 0) kshort = k_scan_block<short_w, false>;
   const unsigned threads_short = 32u * unsigned(short_w);
   const size_t smem = 0;
   int per_sm = 0;
