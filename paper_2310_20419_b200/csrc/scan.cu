@@ -201,6 +201,7 @@ struct ScanArgs {
   int coop_all;  // hubs per cluster below which every hub is walked cooperatively
   int run_max;   // longest leading run of old entries kept in one round (0: off)
   int run_tasks; // task budget of an old-run round per 64 threads
+  int run_min;   // shortest run taken as an old-run round (0: D + 1)
 };
 
 __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned long long removed,
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
         }
         __syncthreads();
         const uint32_t wr = s_run;
-        if (wr > uint32_t(D)) {
+        if (wr >= (g.run_min ? uint32_t(g.run_min) : uint32_t(D) + 1)) {
           if (tid == 0) skips += uint64_t(wr) * (wr - 1) / 2;  // run entries among themselves
           uint32_t nn = 0;
           for (uint32_t b0 = wr; b0 < na; b0 += NT) {
@@ -869,7 +870,7 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
     const uint32_t tot = sm.tot;
     if (tot == 0) break;
     const uint32_t wr = sm.run;
-    if (wr > uint32_t(D)) {
+    if (wr >= (g.run_min ? uint32_t(g.run_min) : uint32_t(D) + 1)) {
       // Old-run round (k_scan_spec's): the run is kept whole, only fresh
       // candidates are tested against it; the owner pops its run entries.
       uint32_t own = 0;
@@ -1443,6 +1444,14 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return v < 1 ? 1 : v;
   }();
   a.run_tasks = run_tasks;
+  // C3 1M: runs of >= 2 entries 2.022 s, >= 3 2.022 s, >= D + 1 2.025 s,
+  // >= 6 2.053 s
+  static const int run_min = [] {
+    const char* e = std::getenv("RNNDG_RUN_MIN");
+    const int v = e ? std::atoi(e) : 2;
+    return v < 0 ? 0 : v;
+  }();
+  a.run_min = run_min;
   // two-warp CTAs for short lists (4-warp CTAs measured slower,
   // profiles/README.md)
   constexpr int short_w = kPushWarps;
