@@ -106,6 +106,7 @@ int rnndg_destroy(rnndg_ctx* c) {
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);
   if (c->stream) cudaStreamDestroy(c->stream);
+  if (c->host_stage) cudaFreeHost(c->host_stage);
   delete c;
   return RNNDG_OK;
 }

@@ -27,6 +27,8 @@
 #define CCCL_IGNORE_DEPRECATED_API
 #include <cub/device/device_radix_sort.cuh>
 #include <vector>
+#include <thread>
+#include <cstring>
 #include <cub/device/device_scan.cuh>
 #include <cub/device/device_segmented_sort.cuh>
 #include <cub/device/device_select.cuh>
@@ -1032,6 +1034,35 @@ void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t
                  elapsed_ms(c->ev[1], c->ev_scan[0]), elapsed_ms(c->ev[1], c->ev_scan[1]));
 }
 
+namespace {
+
+// memcpy of a large host range on several threads (pinned staging -> the
+// caller's pageable arrays)
+void par_copy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kChunk = size_t(8) << 20;
+  const unsigned hw = std::thread::hardware_concurrency();
+  const size_t nt = std::min<size_t>(hw ? hw : 1, std::min<size_t>(16, bytes / kChunk + 1));
+  if (nt <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  std::vector<std::thread> th;
+  const size_t per = (bytes + nt - 1) / nt;
+  for (size_t t = 0; t < nt; ++t) {
+    const size_t a = t * per, b = std::min(bytes, a + per);
+    if (a >= b) break;
+    th.emplace_back([=] {
+      std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, b - a);
+    });
+  }
+  for (auto& x : th) x.join();
+}
+
+}  // namespace
+
+// Graph export (rnnd::AdjacencyGraph as CSR): compacted on the device, copied
+// to a pinned staging area in one pass at PCIe speed, then into the caller's
+// arrays by a multi-threaded memcpy.
 uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,
                    uint8_t* fresh) {
   const uint64_t n = c->nv;
@@ -1040,6 +1071,18 @@ uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,
   uint64_t m = 0;
   RNNDG_CUDA(cudaMemcpyAsync(&m, c->ex_off.p + n, 8, cudaMemcpyDeviceToHost, c->stream));
   RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  if (!(offsets || ids || dists || fresh)) return m;
+  const size_t b_off = offsets ? (n + 1) * 8 : 0, b_ids = ids ? m * 4 : 0,
+               b_d = dists ? m * 4 : 0, b_f = fresh ? m : 0;
+  const size_t total = b_off + b_ids + b_d + b_f;
+  if (total > c->host_stage_bytes) {
+    if (c->host_stage) RNNDG_CUDA(cudaFreeHost(c->host_stage));
+    c->host_stage = nullptr;
+    c->host_stage_bytes = 0;
+    RNNDG_CUDA(cudaHostAlloc(&c->host_stage, total, cudaHostAllocDefault));
+    c->host_stage_bytes = total;
+  }
+  char* st = static_cast<char*>(c->host_stage);
   if (m && (ids || dists || fresh)) {
     c->ex_ids.ensure(m);
     c->ex_dists.ensure(m);
@@ -1047,16 +1090,22 @@ uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,
     RNNDG_LAUNCH(c, k_export, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->ex_off.p, c->ex_ids.p, c->ex_dists.p, c->ex_fresh.p);
     if (ids)
-      RNNDG_CUDA(cudaMemcpyAsync(ids, c->ex_ids.p, m * 4, cudaMemcpyDeviceToHost, c->stream));
+      RNNDG_CUDA(cudaMemcpyAsync(st + b_off, c->ex_ids.p, b_ids, cudaMemcpyDeviceToHost,
+                                 c->stream));
     if (dists)
-      RNNDG_CUDA(cudaMemcpyAsync(dists, c->ex_dists.p, m * 4, cudaMemcpyDeviceToHost, c->stream));
+      RNNDG_CUDA(cudaMemcpyAsync(st + b_off + b_ids, c->ex_dists.p, b_d, cudaMemcpyDeviceToHost,
+                                 c->stream));
     if (fresh)
-      RNNDG_CUDA(cudaMemcpyAsync(fresh, c->ex_fresh.p, m, cudaMemcpyDeviceToHost, c->stream));
+      RNNDG_CUDA(cudaMemcpyAsync(st + b_off + b_ids + b_d, c->ex_fresh.p, b_f,
+                                 cudaMemcpyDeviceToHost, c->stream));
   }
   if (offsets)
-    RNNDG_CUDA(cudaMemcpyAsync(offsets, c->ex_off.p, (n + 1) * 8, cudaMemcpyDeviceToHost,
-                               c->stream));
+    RNNDG_CUDA(cudaMemcpyAsync(st, c->ex_off.p, b_off, cudaMemcpyDeviceToHost, c->stream));
   RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  if (offsets) par_copy(offsets, st, b_off);
+  if (m && ids) par_copy(ids, st + b_off, b_ids);
+  if (m && dists) par_copy(dists, st + b_off + b_ids, b_d);
+  if (m && fresh) par_copy(fresh, st + b_off + b_ids + b_d, b_f);
   return m;
 }
 

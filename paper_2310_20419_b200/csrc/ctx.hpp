@@ -89,6 +89,9 @@ struct rnndg_ctx {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   uint64_t launches = 0;
+  // pinned host staging for graph export (grown on demand, freed in destroy)
+  void* host_stage = nullptr;
+  size_t host_stage_bytes = 0;
 
   // VectorStore (vector_store.hpp:12-20), row-major n x d fp32
   rnndg::DevBuf<float> x_own;

@@ -191,14 +191,16 @@ class Device:
         n = C.c_uint64()
         m = C.c_uint64()
         self.check(self._L.rnndg_graph_size(self.h, C.byref(n), C.byref(m)))
-        off = np.zeros(n.value + 1, np.uint64)
-        ids = np.zeros(max(m.value, 1), np.uint32)
-        dists = np.zeros(max(m.value, 1), np.float32)
-        fresh = np.zeros(max(m.value, 1), np.uint8)
+        mm = m.value
+        off = np.empty(n.value + 1, np.uint64)
+        ids = np.empty(max(mm, 1), np.uint32)
+        dists = np.empty(max(mm, 1), np.float32)
+        fresh = np.empty(max(mm, 1), np.uint8)
         self.check(self._L.rnndg_get_graph(self.h, ptr(off, u64p), ptr(ids, u32p),
                                            ptr(dists, f32p), ptr(fresh, u8p)))
-        mm = m.value
-        return CSR(off, ids[:mm].copy(), dists[:mm].copy(), fresh[:mm].copy())
+        if mm == 0:
+            return CSR(off, ids[:0], dists[:0], fresh[:0])
+        return CSR(off, ids, dists, fresh)
 
 
 @dataclass
