@@ -23,14 +23,16 @@
 // bit-identical to rnnd::l2_sq.  A vertex's rows are pulled into L2 with one
 // bulk prefetch per row (cp.async.bulk.prefetch.L2, UBLKPF) when it starts.
 //
-//   k_scan_spec<2, false, 4>   lists <= hub_threshold() (256): keys + alive
-//                              list in smem, 7 CTAs of 64 threads per SM
-//   k_scan_hub<32, 2, 4>       hub lists, on a second stream concurrently:
-//                              clusters of two 1024-thread CTAs; lists over
-//                              big_hub_threshold() (1024) walked by both CTAs
+//   k_scan_spec<2, false, 3>   lists <= hub_threshold() (256): keys + alive
+//                              list in smem, 6 CTAs of 64 threads per SM;
+//                              D = 3 speculative rounds and old-run rounds
+//   k_scan_hub<32, C, 4>       hub lists, on a second stream concurrently:
+//                              clusters of C = 2 1024-thread CTAs (4 / 8 in
+//                              the tail passes); lists over
+//                              big_hub_threshold() (1024) walked by all CTAs
 //                              of a cluster (longest first), the rest by one
-//   k_scan_spec<32, true, 4>   hub lists, one 1024-thread CTA each
-//                              (RNNDG_HUB=0)
+//   k_scan_spec<32, true, 4>   hub lists, one 1024-thread CTA each (rows
+//                              shorter than 2 KB, or RNNDG_HUB=0)
 //   k_scan_block               the same walk with two steps per round
 //                              (RNNDG_SPEC=0)
 // Variants measured slower and removed (smem-staged rows, TMA-sliced rows, a
