@@ -249,6 +249,10 @@ def run_sharded(args, rank, world, local):
     pinned = torch.empty(data.shape, dtype=torch.float32, pin_memory=True)
     pinned.numpy()[:] = data
     e2e_secs, d2h = 0.0, 0
+    # one untimed pass warms the export staging (pinned host buffer)
+    eng.load(pinned.numpy())
+    SH.sharded_build([eng], tr, n, world, **p)
+    eng.graph()
     for _ in range(args.steps):
         torch.cuda.synchronize()
         dist.barrier()
