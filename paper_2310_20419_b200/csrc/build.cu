@@ -687,7 +687,9 @@ __global__ void __launch_bounds__(kBlock) k_seg_sort_warp(const uint64_t* __rest
   for (uint64_t s = warp; s < nseg; s += nwarps) {
     const uint64_t b = begin[s];
     const uint32_t len = uint32_t(end[s] - b);
-    if (len <= 32) {
+    if (len <= 1) {  // most buckets of a late pass are empty
+      if (len == 1 && lane == 0) kout[b] = kin[b];
+    } else if (len <= 32) {
       uint64_t v = lane < len ? kin[b + lane] : ~0ull;
       for (uint32_t k = 2; k <= 32; k <<= 1) {
         uint64_t p = shfl_xor_u64(v, int(k - 1));
