@@ -449,6 +449,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   constexpr uint32_t kTasks = NT * D;
   __shared__ uint64_t keys_sh[kCap];
   __shared__ uint32_t alive_sh[kCap];
+  __shared__ uint8_t touch_sh[kCap];  // touched flags of a short list
   __shared__ uint32_t tq[kTasks];  // task: list position of the candidate
   __shared__ uint8_t tw[kTasks];   //       which provisional entry (0 .. D-1)
   __shared__ float tres[kTasks];   //       their distance
@@ -475,12 +476,17 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
     const uint64_t base = g.off[u];
     const uint32_t U = g.cnt[u];
     uint64_t* L = g.keys + base;
-    uint8_t* T = g.touch + base;
+    // touched flags (counter only): shared memory for short lists, the
+    // pass-zeroed global scratch for long ones
+    uint8_t* T = kLong ? g.touch + base : touch_sh;
     const uint64_t* K = kLong ? L : keys_sh;
     uint32_t* A = kLong ? g.alive_g + base : alive_sh;
     for (uint32_t j = tid; j < U; j += NT) {
       const uint64_t k = L[j];
-      if (!kLong) keys_sh[j] = k;
+      if (!kLong) {
+        keys_sh[j] = k;
+        touch_sh[j] = 0;
+      }
       A[j] = j;
       if (g.l2pf) prefetch_row_l2(row(k), row_bytes);
     }
