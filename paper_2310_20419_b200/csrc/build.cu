@@ -965,6 +965,7 @@ void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
   c->has_distances = true;
   c->exact_dists = true;
   c->bulk_fresh = true;
+  c->init_fresh = true;
   op_sort_lists(c);  // establish the sorted-list invariant
 }
 

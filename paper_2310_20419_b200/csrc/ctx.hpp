@@ -165,6 +165,7 @@ struct rnndg_ctx {
   // picks the hub-cluster size of the next scan
   uint64_t hubs_prev = ~0ull;
   bool bulk_fresh = true;
+  bool init_fresh = false;  // lists are the random initial lists (all fresh)
   // shard scans since the last rnndg_shard_totals(reset): distance-stage time
   // and the SURVEY 8(d) units, for the sharded bench roofline
   double shard_scan_s = 0.0;

@@ -1463,7 +1463,11 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   // two-warp CTAs for short lists (4-warp CTAs measured slower,
   // profiles/README.md)
   constexpr int short_w = kPushWarps;
-  const int spec = spec_mode();
+  // the first pass over the random initial lists removes ~80% of the
+  // entries, so most provisional entries would be occluded: two per round
+  // there (C3 1M pass 0: 25.1 -> 21 ms)
+  const int spec = c->init_fresh && spec_mode() == 3 ? 2 : spec_mode();
+  c->init_fresh = false;
   // streamed rows L1::no_allocate only for long rows (see ld256)
   const bool na = cfg.stride * sizeof(float) >= kNaMinRowBytes;
   auto kshort = na ? k_scan_spec<short_w, false, 3, true> : k_scan_spec<short_w, false, 3, false>;
