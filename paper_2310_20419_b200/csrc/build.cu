@@ -849,14 +849,16 @@ void merge_and_swap(rnndg_ctx* c, const uint32_t* post_cnt) {
   c->span = total;
 }
 
-// lists longer than this go to the 1024-thread hub kernel (RNNDG_UCAP,
-// at most kScanUcap, the short kernel's shared-memory capacity).  C3 1M:
-// 512 -> 2.51 s, 256 -> 2.46 s, 128 -> 2.56 s, 64 -> 3.25 s per build.
+// lists longer than this go to the hub kernel (RNNDG_UCAP, at most
+// kScanUcap, the short kernel's shared-memory capacity).  C3 1M with one CTA
+// per hub: 512 -> 2.51 s, 256 -> 2.46 s, 128 -> 2.56 s, 64 -> 3.25 s; with
+// the current kernels: 192 -> 2.051 s, 256 -> 1.999 s, 320 -> 1.989 s,
+// 384 -> 1.976 s, 448 -> 1.985 s, 512 -> 2.011 s.
 uint32_t hub_threshold() {
   static const uint32_t v = [] {
     const char* e = std::getenv("RNNDG_UCAP");
-    const int x = e ? std::atoi(e) : 256;
-    return uint32_t(x >= 32 && x <= int(kScanUcap) ? x : 256);
+    const int x = e ? std::atoi(e) : 384;
+    return uint32_t(x >= 32 && x <= int(kScanUcap) ? x : 384);
   }();
   return v;
 }
