@@ -153,7 +153,7 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
       nact += 1;
       maxlen = U > maxlen ? U : maxlen;
       flag = U > ucap ? 2 : 1;
-      if (U > big_cap) {
+      if (U > ucap && U > big_cap) {  // a hub list (never both queues)
         const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kBigCount]), 1u);
         act_list[2 * n - 1 - x] = uint32_t(u);
       } else if (U > ucap) {
