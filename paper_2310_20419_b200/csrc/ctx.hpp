@@ -77,6 +77,7 @@ enum Counter : int {
   kEvalPairs,  // distances evaluated by the scan (incl. speculative ones)
   kEvalHub,    // ... of which by the hub-list kernel
   kBigCount,   // hub lists longer than big_hub_threshold() (cluster-cooperative)
+  kLongShortCount,  // short lists longer than long_short_threshold() (queued first)
   kNumCounters
 };
 

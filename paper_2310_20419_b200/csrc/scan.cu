@@ -464,7 +464,9 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   const uint32_t quad = lane >> 2, chain = lane & 3;
   const Row row = g.row;
   const uint32_t row_bytes = row.stride * 4u;
-  const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount]) : uint32_t(*g.nsmall);
+  // short lists: the long ones (act_list[0 ..)) first, then the rest
+  const uint32_t nls = kLong ? 0u : uint32_t(g.ctr_in[kLongShortCount]);
+  const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount]) : nls + uint32_t(*g.nsmall);
   unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, evals = 0;
 
   for (;;) {
@@ -472,7 +474,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
     __syncthreads();
     const uint32_t a = s_a;
     if (a >= nq) break;
-    const uint32_t u = kLong ? g.act_list[g.n + a] : uint32_t(g.act_small[a]);
+    const uint32_t u = kLong ? g.act_list[g.n + a]
+                             : (a < nls ? g.act_list[a] : uint32_t(g.act_small[a - nls]));
     const uint64_t base = g.off[u];
     const uint32_t U = g.cnt[u];
     uint64_t* L = g.keys + base;
