@@ -457,6 +457,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   __shared__ uint32_t s_a, s_kept;
   __shared__ uint32_t s_tb[D];     // task base of candidates 1 .. D-1
   __shared__ uint32_t s_nm[D];     // their need masks
+  __shared__ uint32_t s_fr[2];     // fresh alive entries at a round's start (by parity)
   __shared__ uint32_t s_run;       // old-run rounds: window length,
   __shared__ uint32_t s_rp[32];    //   its list positions
   __shared__ uint64_t s_rk[32];    //   and keys
@@ -470,7 +471,10 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, evals = 0;
 
   for (;;) {
-    if (tid == 0) s_a = atomicAdd(g.work + (kLong ? 1 : 0), 1u);
+    if (tid == 0) {
+      s_a = atomicAdd(g.work + (kLong ? 1 : 0), 1u);
+      s_fr[0] = 0;
+    }
     __syncthreads();
     const uint32_t a = s_a;
     if (a >= nq) break;
@@ -484,6 +488,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
     uint8_t* T = kLong ? g.touch + base : touch_sh;
     const uint64_t* K = kLong ? L : keys_sh;
     uint32_t* A = kLong ? g.alive_g + base : alive_sh;
+    uint32_t fr0 = 0;
     for (uint32_t j = tid; j < U; j += NT) {
       const uint64_t k = L[j];
       if (!kLong) {
@@ -491,11 +496,17 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
         touch_sh[j] = 0;
       }
       A[j] = j;
+      fr0 += key_fresh(k);
       if (g.l2pf) prefetch_row_l2(row(k), row_bytes);
     }
+    fr0 = __reduce_add_sync(0xffffffffu, fr0);
+    if (lane == 0 && fr0) atomicAdd(&s_fr[0], fr0);
     __syncthreads();
     uint32_t na = U, nk = 0;
+    uint32_t rb = 0;  // round parity: s_fr[rb] = fresh alive now, s_fr[rb ^ 1] = next round's
     while (na) {
+      const uint32_t ftot = s_fr[rb];
+      if (tid == 0) s_fr[rb ^ 1] = 0;  // visible to the batches after the next barrier
       if (g.run_max) {
         // Old-run round.  The alive entries ahead of the first fresh one are
         // all old: each was tested against every earlier kept entry already,
@@ -504,10 +515,6 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
         // the fresh candidates after it need distances, one per run entry.
         // Used when the run is longer than D and its tasks fit the task
         // arrays; otherwise the speculative round below.
-        uint32_t fr = 0;
-        for (uint32_t j = tid; j < na; j += NT) fr += key_fresh(K[A[j]]) ? 1u : 0u;
-        uint32_t ftot;
-        block_excl_scan<W>(fr, wcnt, ftot);
         if (wid == 0) {
           const bool old = lane < na && !key_fresh(K[A[lane]]);
           const unsigned m = ~__ballot_sync(0xffffffffu, old);
@@ -574,6 +581,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
               }
             }
             const bool stay = valid && !gone;
+            const unsigned fm = __ballot_sync(0xffffffffu, stay && vf);
+            if (lane == 0 && fm) atomicAdd(&s_fr[rb ^ 1], uint32_t(__popc(fm)));
             uint32_t nstay;
             const uint32_t r = block_rank<W>(stay, wcnt, nstay);
             if (stay) A[nn + r] = q;
@@ -584,6 +593,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
             for (uint32_t i = 0; i < wr; ++i) L[nk + i] = s_rk[i];  // old already
           nk += wr;
           na = nn;
+          rb ^= 1u;
           __syncthreads();
           continue;
         }
@@ -709,6 +719,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
         }
         // survivors stay alive; kept provisional entries leave the alive list
         const bool stay = valid && !gone && !(ai < De && (kept >> ai & 1u));
+        const unsigned fm = __ballot_sync(0xffffffffu, stay && vf);
+        if (lane == 0 && fm) atomicAdd(&s_fr[rb ^ 1], uint32_t(__popc(fm)));
         uint32_t nstay;
         const uint32_t r = block_rank<W>(stay, wcnt, nstay);
         if (stay) A[nn + r] = q;
@@ -726,6 +738,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
           if (uint32_t(i) < De && (kept >> i & 1u)) ++nk;
       }
       na = nn;
+      rb ^= 1u;
     }
     if (tid == 0) g.post_cnt[u] = nk;
     for (uint32_t j = tid; j < U; j += NT) touched += T[j];
