@@ -779,7 +779,8 @@ struct HubSmem {
   float tres[kTasks];
   uint32_t wcnt[W];
   uint32_t head[2][32];   // first alive positions, pos << 1 | fresh
-  uint32_t na[2], nfr[2]; // alive and fresh-alive counts
+  uint32_t na[2], nfr[2]; // alive and fresh-alive counts (published)
+  uint32_t frc[2];        // this CTA's fresh alive entries at a round's start (by parity)
   uint32_t a, tot, kept, npk, run;
   uint32_t wp[32];        // the merged first positions (pos << 1 | fresh)
   uint32_t tb[D], nm[D];  // fate tasks of w_2 .. w_D
@@ -813,12 +814,21 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
   // rank r owns positions p % cs == r: U / cs of them, plus one while r < U % cs
   uint32_t* A = g.alive_g + base + rank * (U / cs) + (rank < U % cs ? rank : U % cs);
   uint32_t na = U / cs + (rank < U % cs ? 1u : 0u);
+  uint32_t fr0 = 0;
   for (uint32_t i = tid; i < na; i += NT) {
     const uint32_t p = rank + i * cs;
     A[i] = p;
-    if (g.l2pf) prefetch_row_l2(row(L[p]), row_bytes);
+    const uint64_t k = L[p];
+    fr0 += key_fresh(k);
+    if (g.l2pf) prefetch_row_l2(row(k), row_bytes);
   }
-  if (tid == 0) sm.npk = 0;
+  if (tid == 0) {
+    sm.npk = 0;
+    sm.frc[0] = 0;
+  }
+  __syncthreads();
+  fr0 = __reduce_add_sync(0xffffffffu, fr0);
+  if (lane == 0 && fr0) atomicAdd(&sm.frc[0], fr0);
   __syncthreads();
   // heads published per CTA: the first H alive positions of every CTA hold
   // the first H of the whole list (old-run windows are at most H long)
@@ -826,11 +836,9 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
   uint32_t nk = 0, ao = 0;
   for (uint32_t rnd = 0;; ++rnd) {
     const uint32_t buf = rnd & 1u;
-    uint32_t fr = 0;  // fresh alive entries of this CTA
-    if (g.run_max)
-      for (uint32_t j = tid; j < na; j += NT) fr += key_fresh(L[A[ao + j]]) ? 1u : 0u;
-    uint32_t nfr;
-    block_excl_scan<W>(fr, sm.wcnt, nfr);
+    // fresh alive entries of this CTA (kept current by the survivor ballots)
+    const uint32_t nfr = sm.frc[buf];
+    if (tid == 0) sm.frc[buf ^ 1] = 0;
     if (tid < H) {
       uint32_t h = kInf;
       if (tid < na) {
@@ -951,6 +959,8 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
           }
         }
         const bool stay = valid && !gone;
+        const unsigned fm = __ballot_sync(0xffffffffu, stay && vf);
+        if (lane == 0 && fm) atomicAdd(&sm.frc[buf ^ 1], uint32_t(__popc(fm)));
         uint32_t nstay;
         const uint32_t r = block_rank<W>(stay, sm.wcnt, nstay);
         if (stay) A[nn + r] = q;
@@ -1128,6 +1138,8 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
         if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
       }
       const bool stay = valid && !gone;
+      const unsigned fm = __ballot_sync(0xffffffffu, stay && vf);
+      if (lane == 0 && fm) atomicAdd(&sm.frc[buf ^ 1], uint32_t(__popc(fm)));
       uint32_t nstay;
       const uint32_t r = block_rank<W>(stay, sm.wcnt, nstay);
       if (stay) A[nn + r] = q;
