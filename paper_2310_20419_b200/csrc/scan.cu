@@ -225,7 +225,9 @@ __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned
 }
 
 // Order-preserving block-wide compaction index of `pred`; total in `total`.
-template <int W>
+// kTrail = false drops the trailing barrier that lets `wcnt` be reused at
+// once; callers then alternate between two wcnt arrays.
+template <int W, bool kTrail = true>
 __device__ __forceinline__ uint32_t block_rank(bool pred, uint32_t* wcnt, uint32_t& total) {
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
   const unsigned m = __ballot_sync(0xffffffffu, pred);
@@ -239,7 +241,7 @@ __device__ __forceinline__ uint32_t block_rank(bool pred, uint32_t* wcnt, uint32
     tot += c;
   }
   total = tot;
-  __syncthreads();
+  if (kTrail) __syncthreads();
   return before + __popc(m & ((1u << lane) - 1u));
 }
 
@@ -410,7 +412,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_block(ScanArgs g) {
 
 // ------------------------------------------------------------ speculative
 // Order-preserving block-wide exclusive scan of per-thread counts c.
-template <int W>
+template <int W, bool kTrail = true>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t c, uint32_t* wcnt,
                                                     uint32_t& total) {
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
@@ -430,7 +432,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t c, uint32_t* wcnt,
     tot += v;
   }
   total = tot;
-  __syncthreads();
+  if (kTrail) __syncthreads();
   return before + x - c;
 }
 
@@ -453,7 +455,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   __shared__ uint32_t tq[kTasks];  // task: list position of the candidate
   __shared__ uint8_t tw[kTasks];   //       which provisional entry (0 .. D-1)
   __shared__ float tres[kTasks];   //       their distance
-  __shared__ uint32_t wcnt[W];
+  __shared__ uint32_t wcnt[W], wcnt2[W];  // scan / rank partials (alternating, no trailing barriers)
   __shared__ uint32_t s_a, s_kept;
   __shared__ uint32_t s_tb[D];     // task base of candidates 1 .. D-1
   __shared__ uint32_t s_nm[D];     // their need masks
@@ -542,7 +544,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
             const uint64_t vk = valid ? K[q] : 0ull;
             const bool vf = valid && key_fresh(vk);
             uint32_t ntask;
-            const uint32_t tb = block_excl_scan<W>(vf ? wr : 0u, wcnt, ntask);
+            const uint32_t tb = block_excl_scan<W, false>(vf ? wr : 0u, wcnt, ntask);
             evals += tid == 0 ? ntask : 0u;
             if (vf)
               for (uint32_t i = 0; i < wr; ++i) {
@@ -584,10 +586,9 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
             const unsigned fm = __ballot_sync(0xffffffffu, stay && vf);
             if (lane == 0 && fm) atomicAdd(&s_fr[rb ^ 1], uint32_t(__popc(fm)));
             uint32_t nstay;
-            const uint32_t r = block_rank<W>(stay, wcnt, nstay);
+            const uint32_t r = block_rank<W, false>(stay, wcnt2, nstay);
             if (stay) A[nn + r] = q;
             nn += nstay;
-            __syncthreads();
           }
           if (tid == 0)
             for (uint32_t i = 0; i < wr; ++i) L[nk + i] = s_rk[i];  // old already
@@ -622,7 +623,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
         for (int i = 0; i < D; ++i)
           if (uint32_t(i) < lim && (key_fresh(wk[i]) || vf)) nm |= 1u << i;
         uint32_t ntask;
-        const uint32_t tb = block_excl_scan<W>(__popc(nm), wcnt, ntask);
+        const uint32_t tb = block_excl_scan<W, false>(__popc(nm), wcnt, ntask);
         evals += tid == 0 ? ntask : 0u;
         {
           uint32_t t = tb;
@@ -722,11 +723,11 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
         const unsigned fm = __ballot_sync(0xffffffffu, stay && vf);
         if (lane == 0 && fm) atomicAdd(&s_fr[rb ^ 1], uint32_t(__popc(fm)));
         uint32_t nstay;
-        const uint32_t r = block_rank<W>(stay, wcnt, nstay);
+        const uint32_t r = block_rank<W, false>(stay, wcnt2, nstay);
         if (stay) A[nn + r] = q;
         nn += nstay;
-        __syncthreads();
       }
+      __syncthreads();  // compacted alive list and survivor counts complete
       // kept entries, flagged old (builder.cpp:68), in list order
       if (tid == 0) {
 #pragma unroll
