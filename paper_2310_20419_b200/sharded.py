@@ -164,6 +164,9 @@ class DeviceShard:
         key = torch.empty(max(m, 1), dtype=torch.int64, device=f"cuda:{self.device}")
         b = np.ascontiguousarray(bounds, np.uint64)
         counts = np.zeros(len(bounds) - 1, np.uint64)
+        # the library works on its own stream: memory torch hands out may
+        # still be in use by torch-stream work (e.g. the last exchange)
+        torch.cuda.current_stream(self.device).synchronize()
         self._check(self.dev._L.rnndg_shard_export(
             self.dev.h, b.ctypes.data_as(_lib.u64p), len(bounds) - 1,
             C.c_void_p(dst.data_ptr()), C.c_void_p(key.data_ptr()),
@@ -174,6 +177,10 @@ class DeviceShard:
         torch = self.torch
         dst = dst.contiguous().to(f"cuda:{self.device}")
         key = key.contiguous().to(f"cuda:{self.device}")
+        # the records come from torch-stream work (an NCCL all-to-all, a
+        # concatenation): complete it before the library's own stream reads
+        # them (without this the import raced the collective)
+        torch.cuda.current_stream(self.device).synchronize()
         c = _lib.Counts()
         n = C.c_uint64()
         self._check(self.dev._L.rnndg_shard_import(

@@ -135,3 +135,18 @@ def test_device_shards_match_single_device(world, order):
         assert np.array_equal(part.ids, ref.ids[int(ref.offsets[lo]):int(ref.offsets[hi])])
         assert np.array_equal(part.dists.view(np.uint32),
                               ref.dists[int(ref.offsets[lo]):int(ref.offsets[hi])].view(np.uint32))
+
+
+@pytest.mark.gpu
+def test_nccl_transport_matches_single_device():
+    """The bench's N > 1 path end to end at one rank: TorchDistTransport over
+    NCCL, C5 generator prefix (1M rows), identical to the single-context
+    build (tests/nccl_case.py)."""
+    import random
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    port = random.randint(29600, 29900)
+    r = subprocess.run([sys.executable, os.path.join(here, "nccl_case.py"), "1000000", str(port)],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
