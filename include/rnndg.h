@@ -126,7 +126,9 @@ int rnndg_nnd_build(rnndg_ctx* ctx, uint32_t K, uint32_t sample, uint32_t iters,
 /* ---- data (VectorStore, vector_store.hpp:12-20) ---- */
 /* copies n x d row-major fp32 host rows to the device (H2D) */
 int rnndg_set_data(rnndg_ctx* ctx, const float* rows, uint64_t n, uint32_t d);
-/* borrows rows already resident on the context's device */
+/* borrows rows already resident on the context's device.  The library
+   works on its own CUDA stream: the caller must have completed the work that
+   produced the rows (e.g. synchronise its stream) before this call. */
 int rnndg_set_data_device(rnndg_ctx* ctx, const float* rows_dev, uint64_t n,
                           uint32_t d);
 /* replaces rnnd::load_fvecs (dataset.cpp:82-95) + rnndg_set_data: reads an
@@ -216,7 +218,9 @@ int rnndg_shard_stage(rnndg_ctx* ctx, int kind, uint64_t* nrecords);
 int rnndg_shard_export(rnndg_ctx* ctx, const uint64_t* bounds, uint32_t parts,
                        uint32_t* dst_dev, uint64_t* key_dev, uint64_t* counts);
 /* apply received records (DEVICE buffers); INEDGE stages deletions and
- * returns their number in *nstaged; PENDING reports `inserted` */
+ * returns their number in *nstaged; PENDING reports `inserted`.  The records
+ * are read on the library's stream: the caller completes the transfer that
+ * produced them (e.g. synchronises the stream of its collective) first. */
 int rnndg_shard_import(rnndg_ctx* ctx, int kind, const uint32_t* dst_dev,
                        const uint64_t* key_dev, uint64_t nrecords, uint32_t R,
                        rnndg_counts* partial, uint64_t* nstaged);
