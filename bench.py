@@ -139,7 +139,7 @@ class ClockSampler:
 
 
 def store_rows(cfg, n):
-    from paper_2310_20419_b200 import datagen
+    import datagen
     return datagen.rows(cfg.cfg, cfg.seed, 0, n)
 
 
@@ -151,7 +151,7 @@ def run_reference(args, rank, world):
     if rank != 0:
         return
     from oracle import oracle as O
-    from paper_2310_20419_b200 import datagen
+    import datagen
     cfg = datagen.CONFIGS[args.config]
     n = min(args.cpu_sample, cfg.n)
     data = store_rows(cfg, n)
@@ -174,7 +174,7 @@ def run_reference(args, rank, world):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded generator, csrc/datagen.cpp; stands in for GIST1M)",
+        "data": "synthetic (seeded generator, datagen/datagen.cpp; stands in for GIST1M)",
         "config": {"workload": cfg.name, "rows": cfg.n, "dim": cfg.d, "sample_rows": n,
                    "S": 20, "R": 96, "T1": 4, "T2": 15,
                    "parallelism": f"host threads x{cores} (rank 0 only)"},
@@ -217,7 +217,7 @@ def run_sharded(args, rank, world, local):
     exchanged with NCCL all-to-all.  Total work is fixed: strong scaling."""
     import torch
     import torch.distributed as dist
-    from paper_2310_20419_b200 import datagen
+    import datagen
     from paper_2310_20419_b200 import sharded as SH
     cfg = datagen.CONFIGS[args.config]
     n = args.n or cfg.n
@@ -290,7 +290,7 @@ def run_sharded(args, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * max_secs / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded generator, csrc/datagen.cpp; stands in for GIST1M)",
+            "data": "synthetic (seeded generator, datagen/datagen.cpp; stands in for GIST1M)",
             "config": {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96, "T1": 4,
                        "T2": 15, "parallelism": f"vertex-sharded x{world} (NCCL all-to-all)",
                        "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},
@@ -336,7 +336,8 @@ def main():
         run_sharded(args, rank, world, local)
         dist.destroy_process_group()
         return
-    from paper_2310_20419_b200 import _lib, datagen
+    import datagen
+    from paper_2310_20419_b200 import _lib
     from paper_2310_20419_b200 import rnnd as R
 
     cfg = datagen.CONFIGS[args.config]
@@ -442,7 +443,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * max_secs / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded generator, csrc/datagen.cpp; stands in for GIST1M)",
+        "data": "synthetic (seeded generator, datagen/datagen.cpp; stands in for GIST1M)",
         "config": {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96,
                    "T1": 4, "T2": 15, "parallelism": "1gpu",
                    "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},

@@ -1,4 +1,5 @@
-// datagen.cpp -- seeded synthetic inputs for the five BASELINE.json configs.
+// datagen.cpp -- seeded synthetic inputs (libdatagen.so: test/bench input
+// generator, NOT part of the product library librnndg.so) for the five BASELINE.json configs.
 //
 // The paper's datasets (SIFT1M, GIST1M, Deep1M, SIFT20M)
 // are not available; these generators stand in with the shapes, sizes and
@@ -18,7 +19,6 @@
 
 #include <omp.h>
 
-#include "rnndg.h"
 
 namespace {
 
@@ -56,11 +56,11 @@ struct Spec {
 
 Spec spec_of(int cfg) {
   switch (cfg) {
-    case RNNDG_CFG_GMM128: return {128, 64};
-    case RNNDG_CFG_SIFTLIKE: return {128, 1000};
-    case RNNDG_CFG_GISTLIKE: return {960, 500};
-    case RNNDG_CFG_DEEPLIKE: return {96, 2000};
-    case RNNDG_CFG_DEEP10M: return {96, 10000};
+    case 1 /* C1 */: return {128, 64};
+    case 2 /* C2 */: return {128, 1000};
+    case 3 /* C3 */: return {960, 500};
+    case 4 /* C4 */: return {96, 2000};
+    case 5 /* C5 */: return {96, 10000};
     default: return {0, 0};
   }
 }
@@ -197,21 +197,20 @@ void gen_deeplike(uint64_t seed, uint64_t row0, uint64_t nrows, const Spec& sp,
 
 extern "C" {
 
-uint32_t rnndg_synth_dim(int cfg) { return spec_of(cfg).d; }
+uint32_t dg_synth_dim(int cfg) { return spec_of(cfg).d; }
 
-int rnndg_synth(int cfg, uint64_t seed, uint64_t row0, uint64_t nrows,
-                float* out) {
+int dg_synth(int cfg, uint64_t seed, uint64_t row0, uint64_t nrows, float* out) {
   Spec sp = spec_of(cfg);
-  if (sp.d == 0 || (nrows && !out)) return RNNDG_EPARAM;
+  if (sp.d == 0 || (nrows && !out)) return 1;
   switch (cfg) {
-    case RNNDG_CFG_GMM128: gen_gmm(seed, row0, nrows, sp, out); break;
-    case RNNDG_CFG_SIFTLIKE: gen_siftlike(seed, row0, nrows, sp, out); break;
-    case RNNDG_CFG_GISTLIKE: gen_gistlike(seed, row0, nrows, sp, out); break;
-    case RNNDG_CFG_DEEPLIKE:
-    case RNNDG_CFG_DEEP10M: gen_deeplike(seed, row0, nrows, sp, out); break;
-    default: return RNNDG_EPARAM;
+    case 1 /* C1 */: gen_gmm(seed, row0, nrows, sp, out); break;
+    case 2 /* C2 */: gen_siftlike(seed, row0, nrows, sp, out); break;
+    case 3 /* C3 */: gen_gistlike(seed, row0, nrows, sp, out); break;
+    case 4 /* C4 */:
+    case 5 /* C5 */: gen_deeplike(seed, row0, nrows, sp, out); break;
+    default: return 1;
   }
-  return RNNDG_OK;
+  return 0;
 }
 
 }  // extern "C"

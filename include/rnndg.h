@@ -56,13 +56,6 @@ extern "C" {
 #define RNNDG_ENTRY_RANDOM 0
 #define RNNDG_ENTRY_FIXED 1
 
-/* synthetic BASELINE.json configs (datagen.cpp) */
-#define RNNDG_CFG_GMM128 1   /* C1: 20k x 128 GMM, 64 comps, sigma 0.3 */
-#define RNNDG_CFG_SIFTLIKE 2 /* C2: 1M x 128 integer 0..255, ~40% zeros */
-#define RNNDG_CFG_GISTLIKE 3 /* C3: 1M x 960 in [0,1], low-rank clusters */
-#define RNNDG_CFG_DEEPLIKE 4 /* C4: 1M x 96 unit norm, 2,000 comps */
-#define RNNDG_CFG_DEEP10M 5  /* C5: 10M x 96 unit norm, 10,000 comps */
-
 typedef struct rnndg_ctx rnndg_ctx;
 
 /* EditCounts, builder.hpp:25-38 */
@@ -225,11 +218,6 @@ int rnndg_shard_import(rnndg_ctx* ctx, int kind, const uint32_t* dst_dev,
                        const uint64_t* key_dev, uint64_t nrecords, uint32_t R,
                        rnndg_counts* partial, uint64_t* nstaged);
 int rnndg_shard_out_prune(rnndg_ctx* ctx, uint32_t R);
-
-/* ---- synthetic inputs (host, no GPU needed) ---- */
-uint32_t rnndg_synth_dim(int cfg);
-int rnndg_synth(int cfg, uint64_t seed, uint64_t row0, uint64_t nrows,
-                float* out);
 
 #ifdef __cplusplus
 }

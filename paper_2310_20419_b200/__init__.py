@@ -2,7 +2,8 @@
 
 The product is librnndg.so (sm_100a CUDA kernels + host orchestration behind
 the C ABI in include/rnndg.h).  `rnnd` mirrors the reference C++ API on top of
-it; `datagen` exposes the seeded BASELINE.json input generators.
+it.  (The seeded BASELINE.json input generators live outside the product,
+in the top-level `datagen` package.)
 """
 from . import rnnd  # noqa: F401
 from .rnnd import *  # noqa: F401,F403

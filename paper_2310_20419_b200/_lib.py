@@ -96,8 +96,8 @@ def lib() -> C.CDLL:
         "rnndg_nnd_finalize": (C.c_int, [vp]),
         "rnndg_nnd_build": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                       C.c_uint64, C.POINTER(BuildStatsC)]),
-        "rnndg_synth_dim": (C.c_uint32, [C.c_int]),
-        "rnndg_synth": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, f32p]),
+        
+        
     }
     for name, (res, args) in sig.items():
         fn = getattr(L, name)
@@ -118,7 +118,7 @@ EXPORTED = (
     "rnndg_update_pass", "rnndg_reverse", "rnndg_sort_lists", "rnndg_build",
     "rnndg_pass_counts", "rnndg_graph_size", "rnndg_get_graph", "rnndg_set_graph",
     "rnndg_index_bytes", "rnndg_degree_stats", "rnndg_search", "rnndg_brute_force",
-    "rnndg_rng_strategy", "rnndg_l2_pairs", "rnndg_synth_dim", "rnndg_synth",
+    "rnndg_rng_strategy", "rnndg_l2_pairs",
     "rnndg_set_partition", "rnndg_shard_scan", "rnndg_shard_stage", "rnndg_shard_export",
     "rnndg_shard_import", "rnndg_shard_out_prune", "rnndg_shard_totals",
     "rnndg_nnd_init", "rnndg_nnd_pass", "rnndg_nnd_pools", "rnndg_nnd_finalize",

@@ -7,7 +7,7 @@ builds.json  - rnnd::build(threads=4) on small seeded stores: sha256 of the
                serialized RNND index, total EditCounts and per-pass counts.
 search.npz   - rnnd::batch_search / brute_force_gt on one of those graphs.
 Inputs are regenerated at test time (oracle synth_uniform = the reference's
-synth_uniform, or the product's seeded datagen, whose bytes are hashed too).
+synth_uniform, or the seeded datagen package, whose bytes are hashed too).
 """
 import hashlib
 import json
@@ -20,7 +20,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)
 sys.path.insert(0, ROOT)
 
 from oracle import oracle as O  # noqa: E402
-from paper_2310_20419_b200 import datagen  # noqa: E402
+import datagen  # noqa: E402
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 from golden_data import data_for  # noqa: E402
 

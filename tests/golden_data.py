@@ -9,5 +9,5 @@ def data_for(case):
     if case["kind"] == "grid":  # heavy exact ties and duplicate points
         u = O.synth_uniform(case["n"], case["d"], case["data_seed"])
         return (np.round(u * 8.0) / 8.0).astype(np.float32)
-    from paper_2310_20419_b200 import datagen
+    import datagen
     return datagen.rows(case["cfg"], case["data_seed"], 0, case["n"])

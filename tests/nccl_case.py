@@ -16,7 +16,8 @@ sys.path.insert(0, ROOT)
 def main(n: int, port: int) -> int:
     import torch
     import torch.distributed as dist
-    from paper_2310_20419_b200 import datagen, rnnd as R, sharded as SH
+    import datagen
+    from paper_2310_20419_b200 import rnnd as R, sharded as SH
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1")
     torch.cuda.set_device(0)
     dist.init_process_group("nccl", device_id=torch.device("cuda", 0))

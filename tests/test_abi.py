@@ -48,7 +48,7 @@ def test_create_without_gpu_reports_error_code():
 
 
 def test_datagen_deterministic_and_prefix_stable():
-    from paper_2310_20419_b200 import datagen as D
+    import datagen as D
     for c in (D.C1, D.C2, D.C3, D.C4, D.C5):
         a = D.rows(c.cfg, c.seed, 0, 64)
         b = D.rows(c.cfg, c.seed, 0, 64)
@@ -58,7 +58,7 @@ def test_datagen_deterministic_and_prefix_stable():
 
 
 def test_datagen_value_ranges():
-    from paper_2310_20419_b200 import datagen as D
+    import datagen as D
     x = D.base(D.C2, 4000)
     assert x.min() == 0 and x.max() <= 255 and np.all(x == np.round(x))
     assert 0.3 < float((x == 0).mean()) < 0.5  # ~40% zeros
@@ -71,7 +71,7 @@ def test_datagen_value_ranges():
 
 def test_datagen_pinned_bytes():
     """Generator drift would silently change every benchmark input."""
-    from paper_2310_20419_b200 import datagen as D
+    import datagen as D
     got = {c.name: hashlib.sha256(D.rows(c.cfg, c.seed, 0, 256).tobytes()).hexdigest()[:16]
            for c in (D.C1, D.C2, D.C3, D.C4, D.C5)}
     path = os.path.join(ROOT, "tests", "golden", "datagen_sha.txt")

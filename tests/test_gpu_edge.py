@@ -108,7 +108,7 @@ def test_full_size_properties(R, oracle):
     equal to the exact reference l2 of its endpoints (a sample of 20k
     entries, bit-exact), per-pass counter identities (inserted <= removed),
     and determinism (a second build gives identical bytes)."""
-    from paper_2310_20419_b200 import datagen
+    import datagen
     cfg = datagen.CONFIGS["C3-gistlike-1M"]
     data = datagen.rows(cfg.cfg, cfg.seed, 0, cfg.n)
     store = R.VectorStore(data)

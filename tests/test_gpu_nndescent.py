@@ -38,7 +38,7 @@ def oracle_pools(og):
 
 CASES = [  # (name, data, K, sample, pool)
     ("uniform", lambda: O.synth_uniform(300, 6, 5), 8, 6, 0),
-    ("gist-like", lambda: __import__("paper_2310_20419_b200.datagen", fromlist=["x"]).rows(3, 3, 0, 400), 10, 10, 30),
+    ("gist-like", lambda: __import__("datagen").rows(3, 3, 0, 400), 10, 10, 30),
     ("grid-ties", lambda: np.stack(np.meshgrid(np.arange(12), np.arange(12)), -1).reshape(-1, 2).astype(np.float32), 6, 8, 0),
     ("sample>=n", lambda: O.synth_uniform(12, 3, 2), 4, 50, 0),
 ]
@@ -139,7 +139,7 @@ def test_converges_like_reference_test(R):  # test_nndescent.cpp:113-134
 
 @pytest.mark.skipif(not HAVE_REF, reason="oracle/_ref not built")
 def test_recall_not_below_reference(R):
-    from paper_2310_20419_b200 import datagen
+    import datagen
     x = datagen.rows(1, 0, 0, 4000)  # C1 prefix, d = 128
     p = R.NnDescentParams(K=10, sample=10, iters=6, pool=30, seed=42)
     g = R.build_nndescent(R.VectorStore(x), p)

@@ -106,7 +106,7 @@ def step_data(oracle, kind, n, d, s):
         return oracle.synth_uniform(n, d, s)
     if kind == "grid":
         return (np.round(oracle.synth_uniform(n, d, s) * 8.0) / 8.0).astype(np.float32)
-    from paper_2310_20419_b200 import datagen
+    import datagen
     return datagen.rows(int(kind[-1]), s, 0, n)
 
 
@@ -196,7 +196,7 @@ def test_build_matches_reference_fixture(R, case):
 
 @pytest.mark.slow
 def test_build_c1_prefix_vs_oracle(R, oracle):
-    from paper_2310_20419_b200 import datagen
+    import datagen
     data = datagen.rows(1, 0, 0, 8000)
     g = R.build(R.VectorStore(data))
     og = oracle.OracleGraph(data)
@@ -354,7 +354,7 @@ def test_search_matches_reference_golden(R, oracle):
     fx = np.load(os.path.join(GOLDEN, "search.npz"))
     cases = [c for c in load_cases() if c.get("cfg") == 1]
     data = data_for(cases[0])
-    from paper_2310_20419_b200 import datagen
+    import datagen
     q = datagen.rows(1, 0, 3000, 200)
     assert hashlib.sha256(q.tobytes()).digest() == fx["queries_sha256"].tobytes()
     store = R.VectorStore(data)

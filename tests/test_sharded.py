@@ -115,7 +115,7 @@ def test_device_shards_match_single_device(world, order):
     """Real device shards (rnndg_set_partition + rnndg_shard_*) on one GPU,
     records moved in-process: identical graph and counters to the
     single-context build."""
-    from paper_2310_20419_b200 import datagen
+    import datagen
     from paper_2310_20419_b200 import rnnd as R
     data = datagen.rows(4, 4, 0, 3000)  # C4 (Deep-like) generator prefix
     b = SH.ownership_bounds(3000, world)
