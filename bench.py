@@ -10,8 +10,16 @@ store already resident in HBM.  value = L2 dist-evals/s = pair checks
 device time.  e2e = the same metric through the C ABI with host buffers
 (H2D of the store, build, D2H of the graph) in the timed region.
 
---impl reference runs the UNMODIFIED reference (oracle/_ref, rnnd::build with
-all host threads) on a bounded prefix sample of the same store.
+--impl reference runs the UNMODIFIED reference (oracle/_ref) on the same
+full-size store with all host threads, through its own public pass API
+(random_init, update_neighbors, add_reverse_edges: the schedule rnnd::build
+runs, builder.cpp:253-289): one build's 64 phases (init, 60 passes, 3 reverse
+phases) are split into the K timed steps, so the K steps together are one
+full-config build.
+
+--gpus N without torchrun re-launches itself under torch.distributed.run with
+N ranks (one per GPU); --dry checks that plumbing without a GPU (gloo, no
+build).
 """
 from __future__ import annotations
 
@@ -31,7 +39,7 @@ sys.path.insert(0, ROOT)
 
 PEAKS_PATH = os.path.join(ROOT, "MEASURED_PEAKS.json")
 HBM_FALLBACK_GBS = 6650.0
-CPU_SAMPLE_ROWS = 150_000
+CPU_SAMPLE_ROWS = 0  # 0: the full config
 METRIC = "RNN-Descent build L2 dist-evals/s (1M x 960 fp32, S=20 R=96 T1=4 T2=15)"
 
 
@@ -54,7 +62,10 @@ def parse():
     ap.add_argument("--n", type=int, default=0, help="override rows (debug only)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-recall", action="store_true")
-    ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_ROWS)
+    ap.add_argument("--cpu-sample", type=int, default=CPU_SAMPLE_ROWS,
+                    help="rows of the CPU baseline (0 = the full config)")
+    ap.add_argument("--dry", action="store_true",
+                    help="launcher / rank plumbing only (gloo, no GPU, no build)")
     ap.add_argument("--sharded", action="store_true",
                     help="use the vertex-sharded build even at N=1 (checks that path)")
     return ap.parse_args()
@@ -145,63 +156,140 @@ def store_rows(cfg, n):
 
 # ------------------------------------------------------------ reference arm
 
+def build_phases(T1=4, T2=15):
+    """rnnd::build's schedule (builder.cpp:262-281): init, then T1 outer
+    rounds of T2 update passes, a reverse phase after every round but the
+    last."""
+    ph = ["init"]
+    for t1 in range(1, T1 + 1):
+        ph += ["pass"] * T2
+        if t1 != T1:
+            ph.append("reverse")
+    return ph
+
+
 def run_reference(args, rank, world):
-    """The reference's own CPU implementation (oracle/_ref) on a bounded
-    sample; rank 0 only."""
+    """The reference's own CPU implementation (oracle/_ref), rank 0 only, on
+    the full config: one build's phases split over the K timed steps (W
+    warm-up steps run the first phases of a throwaway build)."""
     if rank != 0:
         return
+    # torchrun sets OMP_NUM_THREADS=1 per rank; the reference gets every host
+    # core (read by libgomp when oracle/_ref is first loaded, just below)
+    ncpu = len(os.sched_getaffinity(0))
+    os.environ["OMP_NUM_THREADS"] = str(ncpu)
     from oracle import oracle as O
     import datagen
     cfg = datagen.CONFIGS[args.config]
-    n = min(args.cpu_sample, cfg.n)
-    data = store_rows(cfg, n)
+    n = args.n or cfg.n
     if not O.ref_available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref not built"}))
         return
-    cores = int(O.ref_lib().ref_max_threads())
-    g = O.RefGraph(data)
-    for _ in range(args.warmup):
-        g.build(threads=0)
+    data = store_rows(cfg, n)
+    threads = max(ncpu, 2)  # threads > 1: the deferred variant (builder.cpp:88-139)
+    phases = build_phases()
+
+    def chunks(k):
+        return [(len(phases) * i) // k for i in range(k + 1)]
+
+    state = {"g": None, "i": 0}
+
+    def run_phases(count):
+        """Run the next `count` phases (a new build starts at phase 0)."""
+        checks = 0
+        for _ in range(count):
+            i = state["i"] % len(phases)
+            if i == 0:
+                state["g"] = O.RefGraph(data)
+                assert state["g"].random_init(20, 42) == 0
+            elif phases[i] == "pass":
+                checks += int(state["g"].update_pass(threads=threads)[3])
+            else:
+                assert state["g"].add_reverse_edges(96, threads=threads, order=0) == 0
+            state["i"] += 1
+        return checks
+
+    b = chunks(max(args.steps, 1))
+    if args.warmup:
+        run_phases(min(args.warmup, len(phases)))
+    state["i"] = 0  # the timed steps are one fresh build
     secs, checks = [], []
-    for _ in range(args.steps):
-        rc, st = g.build(threads=0)
-        assert rc == 0
-        secs.append(float(st[0]))
-        checks.append(float(st[6]))
+    for k in range(args.steps):
+        cnt = b[k + 1] - b[k] if args.steps <= len(phases) else 1
+        t = time.perf_counter()
+        c = run_phases(cnt)
+        secs.append(time.perf_counter() - t)
+        checks.append(c)
     value = sum(checks) / sum(secs)
     line = {
-        "impl": "reference", "metric": metric_for(cfg, args.n or cfg.n), "value": value, "unit": "dist-evals/s",
+        "impl": "reference", "metric": metric_for(cfg, n), "value": value, "unit": "dist-evals/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * sum(secs) / len(secs), "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded generator, datagen/datagen.cpp; stands in for GIST1M)",
-        "config": {"workload": cfg.name, "rows": cfg.n, "dim": cfg.d, "sample_rows": n,
-                   "S": 20, "R": 96, "T1": 4, "T2": 15,
-                   "parallelism": f"host threads x{cores} (rank 0 only)"},
-        "cpu_baseline": {"value": value, "unit": "dist-evals/s", "cores": cores,
+        "data": data_desc(cfg),
+        "config": config_of(cfg, n, f"host threads x{threads} (rank 0 only)"),
+        "cpu_baseline": {"value": value, "unit": "dist-evals/s", "cores": threads,
                          "kind": "reference",
-                         "sample": f"rnnd::build(threads={cores}) on the first {n} rows of "
-                                   f"{cfg.name}"},
+                         "what": "unmodified reference (oracle/_ref): random_init + "
+                                 "update_neighbors / add_reverse_edges, threads=%d, the full "
+                                 "config, one build split over the %d timed steps"
+                                 % (threads, args.steps),
+                         "cpu_model": cpu_model()},
         "e2e": {"value": value, "unit": "dist-evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
-        "build_seconds": statistics.median(secs),
+        "build_seconds": sum(secs) * len(phases) / max(b[-1] if args.steps <= len(phases)
+                                                       else args.steps, 1),
     }
     print(json.dumps(line))
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return ""
+
+
+def config_of(cfg, n, parallelism):
+    return {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96, "T1": 4, "T2": 15,
+            "parallelism": parallelism,
+            "l2_policy": ("inputs larger than L2 (store %.2f GB)" if n * cfg.d * 4 > 126e6
+                          else "store fits in L2 (%.2f GB): no flush between steps")
+            % (n * cfg.d * 4 / 1e9)}
+
+
+STANDS_IN = {1: "a 64-component GMM", 2: "SIFT1M", 3: "GIST1M", 4: "Deep1M", 5: "Deep10M"}
+
+
+def data_desc(cfg):
+    return ("synthetic (seeded generator, datagen/datagen.cpp; stands in for %s)"
+            % STANDS_IN.get(cfg.cfg, cfg.name))
+
+
 # ------------------------------------------------------------------ our arm
 
-def cpu_baseline(cfg, sample):
+def cpu_baseline(cfg, sample, n_full):
+    """The unmodified reference's rnnd::build on the box's host cores
+    (BuildStats.seconds, builder.cpp:260-286): the full config by default."""
     from oracle import oracle as O
-    n = min(sample, cfg.n)
+    n = min(sample, n_full) if sample else n_full
     data = store_rows(cfg, n)
     if O.ref_available():
+        cores = max(len(os.sched_getaffinity(0)), 2)
         g = O.RefGraph(data)
-        rc, st = g.build(threads=0)
-        cores = int(O.ref_lib().ref_max_threads())
-        return {"value": float(st[6]) / float(st[0]), "unit": "dist-evals/s", "cores": cores,
-                "kind": "reference", "seconds": float(st[0]),
-                "sample": f"rnnd::build(threads={cores}) on the first {n} rows of {cfg.name}"}
+        rc, st = g.build(threads=cores)
+        assert rc == 0
+        out = {"value": float(st[6]) / float(st[0]), "unit": "dist-evals/s", "cores": cores,
+               "kind": "reference", "seconds": float(st[0]), "pair_checks": float(st[6]),
+               "what": f"rnnd::build(threads={cores}) on {n} rows of {cfg.name}",
+               "cpu_model": cpu_model()}
+        if n != n_full:
+            out["sample"] = f"first {n} rows of {cfg.name}"
+        return out
     g = O.OracleGraph(data)
     t = time.perf_counter()
     rc, pc = g.build()
@@ -290,10 +378,8 @@ def run_sharded(args, rank, world, local):
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": 1e3 * max_secs / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-            "data": "synthetic (seeded generator, datagen/datagen.cpp; stands in for GIST1M)",
-            "config": {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96, "T1": 4,
-                       "T2": 15, "parallelism": f"vertex-sharded x{world} (NCCL all-to-all)",
-                       "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},
+            "data": data_desc(cfg),
+            "config": config_of(cfg, n, f"vertex-sharded x{world} (NCCL all-to-all)"),
             "build_seconds": max_secs / args.steps, "wall_seconds_timed": wall,
             "pair_checks_per_build": checks // args.steps,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
@@ -311,9 +397,73 @@ def run_sharded(args, rank, world, local):
         print_line(line)
 
 
+def free_port() -> int:
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: re-run this command under
+    torch.distributed.run with N ranks on this node (one per GPU)."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    sys.stdout.flush()
+    sys.exit(subprocess.call(cmd))
+
+
+def run_dry(args, rank, world):
+    """Rank plumbing only: gloo process group, one all-reduce, the JSON line
+    from rank 0 (no GPU, no build, no value)."""
+    import torch
+    import torch.distributed as dist
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", str(free_port()))
+    os.environ.setdefault("RANK", str(rank))
+    os.environ.setdefault("WORLD_SIZE", str(world))
+    dist.init_process_group("gloo")
+    t = torch.ones(1)
+    dist.all_reduce(t)
+    if rank == 0:
+        print_line({"metric": METRIC, "value": None, "unit": "dist-evals/s", "n_gpus": world,
+                    "steps": args.steps, "warmup": args.warmup, "dry": True,
+                    "ranks_seen": int(t.item()), "impl": args.impl})
+    dist.destroy_process_group()
+
+
+def parity_vs_reference(R, g, st, cfg, n):
+    """The timed build against the reference's own build of the same bytes
+    (tests/golden/builds_1m.json, made by oracle/_ref rnnd::build)."""
+    import hashlib
+    path = os.path.join(ROOT, "tests", "golden", "builds_1m.json")
+    try:
+        with open(path) as f:
+            gold = json.load(f)["configs"]
+    except Exception:
+        return None
+    for name, gd in gold.items():
+        if gd["config"] == cfg.name and gd["rows"] == n:
+            got = [[int(c.removed), int(c.inserted), int(c.flag_skips), int(c.pair_checks)]
+                   for c in st.pass_counts]
+            return {"config": cfg.name, "rows": n,
+                    "index_equal": hashlib.sha256(R.index_bytes(g)).hexdigest()
+                    == gd["index_sha256"],
+                    "per_pass_counts_equal": got == gd["per_pass"],
+                    "reference": "tests/golden/builds_1m.json[%s] (rnnd::build, %s threads)"
+                                 % (name, gd["ref_threads"])}
+    return None
+
+
 def main():
     args = parse()
     rank, world, local = dist_env()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        self_launch(args)
+    if args.dry:
+        run_dry(args, rank, world)
+        return
     if args.impl == "reference":
         run_reference(args, rank, world)
         return
@@ -365,6 +515,7 @@ def main():
         barrier()
         wall = time.perf_counter() - t0
     launches = dev.launches() - launches0
+    parity = parity_vs_reference(R, g, stats[-1], cfg, n)
     dev_secs = sum(s.seconds for s in stats)
     checks = sum(s.edits.pair_checks for s in stats)
     max_secs = dev_secs
@@ -436,17 +587,15 @@ def main():
 
     cpu = None
     if not args.no_cpu_baseline:
-        cpu = cpu_baseline(cfg, args.cpu_sample)
+        cpu = cpu_baseline(cfg, args.cpu_sample, n)
 
     line = {
         "metric": metric_for(cfg, n), "value": value, "unit": "dist-evals/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * max_secs / args.steps, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32",
-        "data": "synthetic (seeded generator, datagen/datagen.cpp; stands in for GIST1M)",
-        "config": {"workload": cfg.name, "rows": n, "dim": cfg.d, "S": 20, "R": 96,
-                   "T1": 4, "T2": 15, "parallelism": "1gpu",
-                   "l2_policy": "inputs larger than L2 (store %.2f GB)" % (data.nbytes / 1e9)},
+        "data": data_desc(cfg),
+        "config": config_of(cfg, n, "1gpu"),
         "build_seconds": max_secs / args.steps,
         "wall_seconds_timed": wall,
         "pair_checks_per_build": stats[-1].edits.pair_checks,
@@ -465,6 +614,7 @@ def main():
         "gpu_launches": launches,
         "clocks": clk.summary(),
         "recall": recall,
+        "parity": parity,
     }
     print(json.dumps(line))
 

@@ -5,6 +5,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -40,6 +41,12 @@ void need_data(rnndg_ctx* c) {
 void need_graph(rnndg_ctx* c) {
   need_data(c);
   if (!c->has_graph) throw ParamError("no graph on the context");
+}
+// whole-graph entry points index [0, n) arrays: not on a vertex shard
+// (rnndg_set_partition); the shard protocol has its own rnndg_shard_* calls
+void need_whole(rnndg_ctx* c, const char* what) {
+  if (c->partitioned)
+    throw ParamError(std::string(what) + ": not available on a partitioned context");
 }
 
 // zlib crc32 (graph.cpp:41-43): IEEE 802.3, reflected polynomial 0xEDB88320
@@ -249,6 +256,7 @@ int rnndg_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
 int rnndg_update_pass(rnndg_ctx* c, rnndg_counts* out) {
   return guarded(c, [&] {
     need_graph(c);
+    need_whole(c, "update_neighbors");
     if (!c->has_distances) throw ParamError("update_neighbors: graph has no distances");
     rnndg_counts cc{};
     op_update_pass(c, &cc, nullptr, nullptr, nullptr, nullptr, nullptr);
@@ -259,6 +267,7 @@ int rnndg_update_pass(rnndg_ctx* c, rnndg_counts* out) {
 int rnndg_reverse(rnndg_ctx* c, uint32_t R, int order) {
   return guarded(c, [&] {
     need_graph(c);
+    need_whole(c, "add_reverse_edges");
     op_reverse(c, R, order);
     RNNDG_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -267,6 +276,7 @@ int rnndg_reverse(rnndg_ctx* c, uint32_t R, int order) {
 int rnndg_sort_lists(rnndg_ctx* c) {
   return guarded(c, [&] {
     need_graph(c);
+    need_whole(c, "sort_lists");
     op_sort_lists(c);
     RNNDG_CUDA(cudaStreamSynchronize(c->stream));
   });
@@ -277,6 +287,7 @@ int rnndg_build(rnndg_ctx* c, uint32_t S, uint32_t R, uint32_t T1, uint32_t T2,
                 rnndg_progress_fn progress, void* user) {
   return guarded(c, [&] {
     need_data(c);
+    need_whole(c, "build");
     // builder.cpp:255-258
     if (c->n < 2) throw ParamError("build: need at least 2 vectors");
     if (S < 1 || S > c->n - 1) throw ParamError("build: S out of [1, n-1]");
@@ -413,6 +424,7 @@ int rnndg_set_graph(rnndg_ctx* c, uint64_t n, const uint64_t* offsets, const uin
 int rnndg_index_bytes(rnndg_ctx* c, uint8_t* buf, uint64_t* size) {
   return guarded(c, [&] {
     need_graph(c);
+    need_whole(c, "index_bytes");
     const uint64_t m = op_export(c, nullptr, nullptr, nullptr, nullptr);
     const uint64_t total = 16 + (c->nv + 1) * 8 + m * 4 + 4;
     if (size) *size = total;
@@ -443,6 +455,7 @@ int rnndg_index_bytes(rnndg_ctx* c, uint8_t* buf, uint64_t* size) {
 int rnndg_degree_stats(rnndg_ctx* c, uint32_t cap, uint64_t out[3]) {
   return guarded(c, [&] {
     need_graph(c);
+    need_whole(c, "degree_stats");
     op_degree_stats(c, cap, out);
   });
 }
@@ -453,6 +466,7 @@ int rnndg_search(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t L, ui
                  uint64_t* dist_comps) {
   return guarded(c, [&] {
     need_graph(c);
+    need_whole(c, "search");
     op_search(c, queries, nq, L, K, k, entry_mode, entry_vertex, entry_count, seed, ids,
               dists, visited, dist_comps);
   });

@@ -1320,6 +1320,9 @@ uint64_t op_shard_import(rnndg_ctx* c, int kind, const uint32_t* dst_dev, const 
                          uint64_t nr, uint32_t R, rnndg_counts* partial) {
   const uint64_t n = c->nv;
   ensure_scratch(c);
+  // only an INEDGE import stages records; nothing is left to export after
+  // the others (rnndg_shard_export then reports zero records)
+  if (kind != RNNDG_X_INEDGE) c->rec_n = 0;
   if (kind == RNNDG_X_DELETE) {
     if (nr) {
       c->rec_key2.ensure(nr);

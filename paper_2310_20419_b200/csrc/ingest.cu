@@ -79,6 +79,18 @@ void op_load_fvecs(rnndg_ctx* c, const char* path_c, uint64_t* n_out, uint32_t* 
   const uint64_t rest = size % rec;
   if (nfull >= (1ull << 31)) throw ParamError("load_fvecs: n must be < 2^31");
 
+  // The store is replaced in place: invalidate the context first, so a
+  // DataError part-way through the file (non-finite value, dimension
+  // mismatch, truncated payload) leaves no store and no graph behind (later
+  // calls fail with RNNDG_EPARAM) instead of a half-overwritten store or a
+  // pointer into a buffer ensure() has just reallocated.
+  c->x = nullptr;
+  c->n = 0;
+  c->nv = 0;
+  c->v0 = 0;
+  c->partitioned = false;
+  c->has_graph = false;
+  c->xp_src = nullptr;
   c->x_own.ensure(nfull ? nfull * dim : 1);
   float* dst = c->x_own.p;
   const uint64_t chunk_rows = kChunkBytes / rec > 0 ? kChunkBytes / rec : 1;

@@ -27,6 +27,7 @@ from __future__ import annotations
 
 import ctypes as C
 import enum
+import weakref
 import os
 import time
 from dataclasses import dataclass, field
@@ -145,6 +146,25 @@ class Device:
             _raise(rc, f"rnndg_create(device={device}) failed")
         self.h = h
         self.store_ref = None
+        self._owner = None  # weakref: the AdjacencyGraph held in the graph slot
+
+    # A context has one graph slot.  The graph whose newest state lives there
+    # is its owner; anything that replaces the slot (another build, a store
+    # change, binding another graph) first downloads the owner's state to its
+    # host copy, so graphs built on the same Device stay independent values
+    # (rnnd::build returns the graph by value, builder.hpp:84-86).
+    def _evict(self, keep=None):
+        o = self._owner() if self._owner is not None else None
+        self._owner = None
+        if o is not None and o is not keep and o._dev is self and o._dev_fresh:
+            o._csr = self.get_graph()
+            o._dev_fresh = False
+        if o is keep and o is not None:
+            self._owner = weakref.ref(o)
+
+    def _adopt(self, g: "AdjacencyGraph"):
+        g._dev, g._dev_fresh = self, True
+        self._owner = weakref.ref(g)
 
     def close(self):
         if getattr(self, "h", None):
@@ -166,6 +186,9 @@ class Device:
         return int(self._L.rnndg_kernel_launches(self.h))
 
     def set_data(self, store: VectorStore):
+        if isinstance(store, DeviceStore):  # only its own load puts it on the device
+            raise ParamError("no vector data: this device store was replaced or its load failed")
+        self._evict()
         self.check(self._L.rnndg_set_data(self.h, ptr(store.data, f32p), store.n, store.d))
         self.store_ref = store
 
@@ -176,6 +199,8 @@ class Device:
         build() / batch_search() in place of a VectorStore."""
         n = C.c_uint64()
         d = C.c_uint32()
+        self._evict()
+        self.store_ref = None  # a failed load leaves no store (rnndg_load_fvecs)
         self.check(self._L.rnndg_load_fvecs(self.h, os.fsencode(path), C.byref(n), C.byref(d)))
         ds = DeviceStore(int(n.value), int(d.value), self)
         self.store_ref = ds
@@ -261,14 +286,18 @@ class AdjacencyGraph:
         """Device context holding `store` and this graph."""
         if self._dev is None:
             self._dev = Device()
-        if self._dev.store_ref is not store:
+        dev = self._dev
+        owner = dev._owner() if dev._owner is not None else None
+        if dev.store_ref is not store:
             csr = self._host()
-            self._dev.set_data(store)
-            self._dev.set_graph(csr, self.has_distances)
-        elif not self._dev_fresh:
-            self._dev.set_graph(self._host(), self.has_distances)
-        self._dev_fresh = True
-        return self._dev
+            dev.set_data(store)  # evicts the slot's owner
+            dev.set_graph(csr, self.has_distances)
+        elif owner is not self or not self._dev_fresh:
+            csr = self._host()
+            dev._evict(keep=None)
+            dev.set_graph(csr, self.has_distances)
+        dev._adopt(self)
+        return dev
 
     def size(self) -> int:
         return len(self._host().offsets) - 1
@@ -362,7 +391,7 @@ def random_init(store: VectorStore, S: int, seed: int) -> AdjacencyGraph:
     dev = Device()
     dev.set_data(store)
     dev.check(dev._L.rnndg_random_init(dev.h, S, seed))
-    g._dev, g._dev_fresh, g.has_distances = dev, True, True
+    dev._adopt(g)
     return g
 
 
@@ -411,11 +440,12 @@ def build(store: VectorStore, params: BuildParams = BuildParams(),
         cb = _lib.PROGRESS_FN(_cb)
     else:
         cb = _lib.PROGRESS_FN()
+    dev._evict()
     dev.check(dev._L.rnndg_build(dev.h, params.S, params.R, params.T1, params.T2,
                                  params.seed, int(params.prune_order), C.byref(st), cb,
                                  None))
     g = AdjacencyGraph(store.n)
-    g._dev, g._dev_fresh, g.has_distances = dev, True, True
+    dev._adopt(g)
     if stats is not None:
         stats.seconds = st.seconds
         stats.update_passes = st.update_passes
@@ -466,6 +496,7 @@ class NnDescent:
 
     def init(self):
         p = self.params
+        self.dev._evict()  # the init reuses the graph slot (random_init)
         self.dev.check(self.dev._L.rnndg_nnd_init(self.dev.h, p.K, p.sample, p.iters, p.pool,
                                                   p.seed))
         self._initialised = True
@@ -493,7 +524,7 @@ class NnDescent:
     def finalize(self) -> "AdjacencyGraph":
         self.dev.check(self.dev._L.rnndg_nnd_finalize(self.dev.h))
         g = AdjacencyGraph(self.store.n)
-        g._dev, g._dev_fresh, g.has_distances = self.dev, True, True
+        self.dev._adopt(g)
         return g
 
 
@@ -507,10 +538,11 @@ def build_nndescent(store, params: NnDescentParams = NnDescentParams(),
     if dev.store_ref is not store:
         dev.set_data(store)
     st = _lib.BuildStatsC()
+    dev._evict()
     dev.check(dev._L.rnndg_nnd_build(dev.h, params.K, params.sample, params.iters, params.pool,
                                      params.seed, C.byref(st)))
     g = AdjacencyGraph(store.n)
-    g._dev, g._dev_fresh, g.has_distances = dev, True, True
+    dev._adopt(g)
     if stats is not None:
         stats.seconds = st.seconds
         stats.update_passes = st.update_passes

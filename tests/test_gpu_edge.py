@@ -100,6 +100,32 @@ def test_seed_changes_graph_deterministically(R, oracle):
     assert R.index_bytes(a) != R.index_bytes(b)
 
 
+def test_graphs_on_one_device_are_independent_values(R, oracle):
+    """rnnd::build returns the graph by value (builder.hpp:84-86): a second
+    build, an update pass or a store change on the same Device must not
+    change a graph built earlier on it."""
+    data = oracle.synth_uniform(400, 8, 7)
+    store = R.VectorStore(data)
+    dev = R.Device()
+    dev.set_data(store)
+    g1 = R.build(store, R.BuildParams(S=10, R=12, T1=2, T2=3, seed=1), device=dev)
+    g2 = R.build(store, R.BuildParams(S=10, R=12, T1=2, T2=3, seed=2), device=dev)
+    og1, og2 = oracle.OracleGraph(data), oracle.OracleGraph(data)
+    og1.build(S=10, R=12, T1=2, T2=3, seed=1)
+    og2.build(S=10, R=12, T1=2, T2=3, seed=2)
+    assert R.index_bytes(g1) == og1.index_bytes()
+    assert R.index_bytes(g2) == og2.index_bytes()
+    # an update pass on g1 leaves g2 alone, and g1 sees its own pass
+    before = R.index_bytes(g2)
+    R.update_neighbors(g1, store)
+    assert R.index_bytes(g2) == before
+    og1.update_pass()
+    assert g1.csr.offsets.tolist() == og1.export().offsets.tolist()
+    # a store change on the Device keeps both graphs
+    dev.set_data(R.VectorStore(data[:50].copy()))
+    assert R.index_bytes(g2) == before
+
+
 @pytest.mark.slow
 def test_full_size_properties(R, oracle):
     """BASELINE C3 at full size (1M x 960): too large for the oracle, so the
