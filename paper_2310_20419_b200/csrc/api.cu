@@ -136,6 +136,7 @@ int rnndg_set_data(rnndg_ctx* c, const float* rows, uint64_t n, uint32_t d) {
     c->nv = n;
     c->partitioned = false;
     c->has_graph = false;
+    c->pending = false;
     c->xp_src = nullptr;  // chain-blocked copy is stale
   });
 }
@@ -241,6 +242,7 @@ int rnndg_set_data_device(rnndg_ctx* c, const float* rows_dev, uint64_t n, uint3
     c->nv = n;
     c->partitioned = false;
     c->has_graph = false;
+    c->pending = false;
     c->xp_src = nullptr;
   });
 }
@@ -260,6 +262,8 @@ int rnndg_update_pass(rnndg_ctx* c, rnndg_counts* out) {
     if (!c->has_distances) throw ParamError("update_neighbors: graph has no distances");
     rnndg_counts cc{};
     op_update_pass(c, &cc, nullptr, nullptr, nullptr, nullptr, nullptr);
+    materialize_pending(c);  // the caller's graph carries exact distances
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
     if (out) *out = cc;
   });
 }
@@ -335,7 +339,9 @@ int rnndg_build(rnndg_ctx* c, uint32_t S, uint32_t R, uint32_t T1, uint32_t T2,
       }
     }
     // builder.cpp:283-285 sorts every list nearest-first: the device lists
-    // are always sorted (build.cu invariant), so there is nothing left to do
+    // are sorted (build.cu invariant) once the last pass's pending redirect
+    // distances are resolved
+    materialize_pending(c);
     RNNDG_CUDA(cudaEventRecord(c->ev[5], c->stream));
     RNNDG_CUDA(cudaEventSynchronize(c->ev[5]));
     float ms = 0.f;
@@ -411,6 +417,7 @@ int rnndg_set_graph(rnndg_ctx* c, uint64_t n, const uint64_t* offsets, const uin
     RNNDG_CUDA(cudaStreamSynchronize(c->stream));
     c->span = m;
     c->has_graph = true;
+    c->pending = false;
     c->has_distances = dists != nullptr;
     c->exact_dists = false;  // caller-provided distances: id-based membership
     // graphs with cached distances keep every list sorted by (dist, id)

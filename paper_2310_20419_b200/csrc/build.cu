@@ -42,6 +42,7 @@
 #include "common.cuh"
 #include "ctx.hpp"
 #include "scan.cuh"
+#include "quad.cuh"
 
 namespace rnndg {
 
@@ -134,7 +135,10 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
                                                     uint32_t* __restrict__ post_cnt,
                                                                           unsigned long long* __restrict__ ctr,
                                                     uint32_t ucap, uint32_t big_cap,
-                                                    uint32_t ls_cap) {
+                                                    uint32_t ls_cap, uint32_t gcap,
+                                                    uint32_t* __restrict__ gq,
+                                                    uint64_t* __restrict__ mat_b,
+                                                    uint64_t* __restrict__ mat_e) {
   const uint32_t lane = lane_id();
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -148,13 +152,25 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
       act = __any_sync(0xffffffffu, j < U && key_fresh(key[b + j]));
     }
     if (lane != 0) continue;
+    if (mat_b) {
+      // an active list the Gram walk does not take, ending in pending
+      // entries (they sort last): its distances are resolved before the scan
+      const bool need = act && U > gcap && U && key_pending(key[b + U - 1]);
+      mat_b[u] = need ? b : 0;
+      mat_e[u] = need ? b + U : 0;
+    }
     uint8_t flag = 0;
     if (act) {
       aentries += U;
       nact += 1;
       maxlen = U > maxlen ? U : maxlen;
       flag = U > ucap ? 2 : (U > ls_cap ? 3 : 1);
-      if (flag == 3) {  // long short list: queued ahead of the others, act_list[i]
+      if (U <= gcap) {  // Gram-filtered walk (gram.cu), queued by size class
+        const int gc = U <= 16 ? 0 : (U <= 32 ? 1 : (U <= 64 ? 2 : 3));
+        const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kGram0 + gc]), 1u);
+        gq[uint64_t(gc) * n + x] = uint32_t(u);
+        flag = 4;
+      } else if (flag == 3) {  // long short list: queued ahead of the others, act_list[i]
         const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLongShortCount]), 1u);
         act_list[x] = uint32_t(u);
       } else if (U > ucap && U > big_cap) {  // a hub list (never both queues)
@@ -243,16 +259,19 @@ __global__ void k_pend_scatter(uint64_t span, const uint32_t* __restrict__ pend_
 // vertex, on a bucket sorted by key.  A proposal is dropped when it equals the
 // previous proposal (duplicate redirects carry bit-identical keys, so keeping
 // one equals the reference's sort + unique) or when the post list already
-// holds the same (dist, id) -- or, when the cached distances came from the
-// caller and are not known to be exact, the same id (has_target,
-// builder.cpp:22-26).  brank = exclusive rank among kept proposals.
+// holds its id (has_target, builder.cpp:22-26).  by_id = 0: every key is exact
+// (reverse proposals on materialised lists), so the id test is a binary
+// search for the same (dist, id); by_id = 1: redirect records carry pending
+// distances (gram.cu) or the cached distances came from the caller, so the
+// warp compares ids against the whole post list, 32 at a time.  brank =
+// exclusive rank among kept proposals.
 __global__ void __launch_bounds__(kBlock)
     k_apply_count(uint64_t n, const uint64_t* __restrict__ off,
                   const uint64_t* __restrict__ key, const uint32_t* __restrict__ post_cnt,
                   const uint64_t* __restrict__ boff, const uint64_t* __restrict__ bkey,
                   uint8_t* __restrict__ bflag, uint32_t* __restrict__ brank,
                   uint32_t* __restrict__ new_cnt, unsigned long long* __restrict__ ctr,
-                  int count_inserted, int exact) {
+                  int count_inserted, int by_id) {
   const uint32_t lane = lane_id();
   unsigned long long inserted = 0;
   WARP_LOOP(u, n) {
@@ -266,25 +285,22 @@ __global__ void __launch_bounds__(kBlock)
     uint32_t ins = 0;
     for (uint64_t xb = b0; xb < b1; xb += 32) {
       const uint64_t xi = xb + lane;
-      bool keep = false;
-      if (xi < b1) {
-        const uint64_t k = bkey[xi];
-        const bool dup = xi > b0 && bkey[xi - 1] == k;
-        bool present = false;
-        if (!dup) {
-          if (exact) {
-            const uint32_t pos = lower_bound(P, pc, k & ~1ull);
-            present = pos < pc && (P[pos] >> 1) == (k >> 1);
-          } else {
-            // caller-provided distances: match on the id alone, exactly as
-            // has_target (builder.cpp:22-26)
-            const uint32_t id = key_id(k);
-            for (uint32_t j = 0; j < pc && !present; ++j) present = key_id(P[j]) == id;
-          }
+      const uint64_t k = xi < b1 ? bkey[xi] : kTomb;
+      const bool dup = xi < b1 && xi > b0 && bkey[xi - 1] == k;
+      bool present = false;
+      if (by_id) {
+        const uint32_t id = key_id(k);
+        for (uint32_t j0 = 0; j0 < pc; j0 += 32) {
+          const uint32_t pid = j0 + lane < pc ? key_id(P[j0 + lane]) : kNone;
+#pragma unroll 8
+          for (int q = 0; q < 32; ++q) present |= __shfl_sync(0xffffffffu, pid, q) == id;
         }
-        keep = !dup && !present;
-        bflag[xi] = keep ? 0 : 1;
+      } else if (xi < b1 && !dup) {
+        const uint32_t pos = lower_bound(P, pc, k & ~1ull);
+        present = pos < pc && (P[pos] >> 1) == (k >> 1);
       }
+      const bool keep = xi < b1 && !dup && !present;
+      if (xi < b1) bflag[xi] = keep ? 0 : 1;
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       if (xi < b1) brank[xi] = ins + __popc(m & ((1u << lane) - 1));
       ins += __popc(m);
@@ -820,6 +836,7 @@ void ensure_scratch(rnndg_ctx* c) {
   c->label.ensure(2 * n);
   c->okey.ensure(2 * n);
   c->act_small.ensure(n);
+  c->gram_q.ensure(4 * n + 1);
   c->key_s.ensure(span);
   c->pend_src.ensure(span);
   c->pend_key.ensure(span);
@@ -982,12 +999,65 @@ void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
     launch_init_dists(c, S);
   }
   c->has_graph = true;
+  c->pending = false;
   c->has_distances = true;
   c->exact_dists = true;
   c->bulk_fresh = true;
   c->init_fresh = true;
   op_sort_lists(c);  // establish the sorted-list invariant
 }
+
+// ------------------------------------------------------ pending distances
+// Redirected entries arrive with a pending distance (gram.cu item 5).  The
+// Gram walk computes them while streaming the list; everywhere else they are
+// resolved here: exact l2_sq(u, v) by a quad per pending entry (quad.cuh,
+// bit-identical to rnnd::l2_sq), then the list re-sorted.  [mat_b[u],
+// mat_e[u]) is the list of u when it needs it, else empty.
+__global__ void __launch_bounds__(kBlock)
+    k_mark_pending(uint64_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ cnt,
+                   const uint64_t* __restrict__ key, uint64_t* __restrict__ mat_b,
+                   uint64_t* __restrict__ mat_e) {
+  for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
+       u += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t b = off[u];
+    const uint32_t U = cnt[u];
+    const bool need = U && key_pending(key[b + U - 1]);
+    mat_b[u] = need ? b : 0;
+    mat_e[u] = need ? b + U : 0;
+  }
+}
+
+__global__ void __launch_bounds__(kBlock)
+    k_resolve_pending(uint64_t n, uint64_t v0, const uint64_t* __restrict__ mat_b,
+                      const uint64_t* __restrict__ mat_e, uint64_t* __restrict__ key, Row row) {
+  __shared__ uint32_t q[kWarpsPerBlock][32];
+  const uint32_t lane = lane_id(), wib = threadIdx.x >> 5, quad = lane >> 2, chain = lane & 3;
+  WARP_LOOP(u, n) {
+    const uint64_t b = mat_b[u], e = mat_e[u];
+    if (b == e) continue;
+    const float* xu = row.xp + (v0 + u) * row.stride;
+    for (uint64_t j0 = b; j0 < e; j0 += 32) {
+      const bool pend = j0 + lane < e && key_pending(key[j0 + lane]);
+      const unsigned m = __ballot_sync(0xffffffffu, pend);
+      if (pend) q[wib][__popc(m & ((1u << lane) - 1u))] = uint32_t(j0 + lane - b);
+      __syncwarp();
+      const uint32_t np = __popc(m);
+      for (uint32_t k0 = 0; k0 < np; k0 += 8) {
+        const uint32_t k = k0 + quad;
+        const uint64_t slot = b + q[wib][k < np ? k : k0];
+        const uint64_t kv = key[slot];
+        const float d = quad_l2<false>(row.xp + uint64_t(key_id(kv)) * row.stride, xu, chain,
+                                       row.nblk, row.ntail);
+        if (k < np && chain == 0) key[slot] = make_key(d, key_id(kv), key_fresh(kv));
+      }
+      __syncwarp();
+    }
+  }
+}
+
+namespace {
+void resolve_pending(rnndg_ctx* c);
+}  // namespace
 
 // Scan phase of a pass: counters zeroed, active vertices marked, locality
 // order, distance stage.  Redirects end up in pend_src/pend_key by slot.
@@ -1005,7 +1075,12 @@ void op_scan_phase(rnndg_ctx* c) {
   if (n)
     RNNDG_LAUNCH(c, k_mark_active, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
-                 big_hub_threshold(c), long_short_threshold());
+                 big_hub_threshold(c), long_short_threshold(), gram_cap(), c->gram_q.p,
+                 c->pending ? c->mat_b.ensure(n) : nullptr, c->pending ? c->mat_e.ensure(n) : nullptr);
+  if (c->pending && n) {
+    prepare_chain_layout(c);
+    resolve_pending(c);
+  }
   locality_order(c);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
   launch_scan(c, c->work.p);
@@ -1023,7 +1098,9 @@ void op_apply_local(rnndg_ctx* c) {
   sort_buckets(c, c->span);
   RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p,
                c->post_cnt.p, c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, ctr, 1,
-               int(c->exact_dists));
+               int(gram_cap() != 0 || !c->exact_dists));
+  // redirect records carry pending distances when the Gram walk is on
+  if (gram_cap()) c->pending = true;
   merge_and_swap(c, c->post_cnt.p);
 }
 
@@ -1049,12 +1126,16 @@ void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t
     std::fprintf(stderr,
                  "[rnndg] pass active=%llu large=%llu maxlen=%llu entries=%llu checks=%llu "
                  "evals=%llu hub_evals=%llu removed=%llu inserted=%llu touched=%llu "
-                 "order=%.3fms scan=%.3fms apply=%.3fms hubk=%.3fms shortk=%.3fms\n",
+                 "order=%.3fms scan=%.3fms apply=%.3fms hubk=%.3fms shortk=%.3fms "
+                 "gram=%llu/%llu/%llu/%llu amb=%llu exact=%llu gramk=%.3fms\n",
                  h[kActiveCount], h[kLargeCount] + h[kBigCount], h[kMaxLen], h[kActiveEntries], h[kPairChecks],
                  h[kEvalPairs], h[kEvalHub],
                  h[kRemoved], h[kInserted], h[kTouched], elapsed_ms(c->ev[0], c->ev[1]),
                  elapsed_ms(c->ev[1], c->ev[2]), elapsed_ms(c->ev[2], c->ev[3]),
-                 elapsed_ms(c->ev[1], c->ev_scan[0]), elapsed_ms(c->ev[1], c->ev_scan[1]));
+                 elapsed_ms(c->ev[1], c->ev_scan[0]), elapsed_ms(c->ev[1], c->ev_scan[1]),
+                 h[kGram0], h[kGram1], h[kGram2], h[kGram3], h[kGramAmb], h[kGramExact],
+                 gram_cap() ? elapsed_ms(c->ev[1], c->ev_scan[2]) : 0.f);
+  if (c->trace) gram_trace(c);
 }
 
 namespace {
@@ -1088,6 +1169,7 @@ void par_copy(void* dst, const void* src, size_t bytes) {
 // arrays by a multi-threaded memcpy.
 uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,
                    uint8_t* fresh) {
+  materialize_pending(c);
   const uint64_t n = c->nv;
   c->ex_off.ensure(n + 1);
   scan_u32(c, c->cnt.p, c->ex_off.p, n);
@@ -1184,6 +1266,7 @@ void in_prune(rnndg_ctx* c, uint32_t R) {
 void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
   if (R < 1) throw ParamError("add_reverse_edges: R must be >= 1");
   if (!c->has_distances) throw ParamError("add_reverse_edges: graph has no distances");
+  materialize_pending(c);
   c->bulk_fresh = true;
   const uint64_t n = c->nv;
   ensure_scratch(c);
@@ -1204,7 +1287,7 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
   // 2. append-if-absent (no duplicates among reversals: edges are unique)
   RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p, c->cnt.p,
                c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, c->counters.p, 0,
-               int(c->exact_dists));
+               int(!c->exact_dists));
   merge_and_swap(c, c->cnt.p);
   ensure_scratch(c);  // span grew
   // 3. degree caps (builder.cpp:244-250)
@@ -1217,7 +1300,32 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
   }
 }
 
+namespace {
+// exact distances of the pending entries of the lists marked in mat_b /
+// mat_e, then those lists re-sorted in place
+void resolve_pending(rnndg_ctx* c) {
+  const uint64_t n = c->nv;
+  const ScanConfig cfg = scan_config(c);
+  RNNDG_LAUNCH(c, k_resolve_pending, warp_grid(c, n), kBlock, 0, n, c->v0, c->mat_b.p,
+               c->mat_e.p, c->key.p, Row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail});
+  seg_sort_keys(c, c->key.p, c->key.p, c->span, n, c->mat_b.p, c->mat_e.p);
+}
+}  // namespace
+
+void materialize_pending(rnndg_ctx* c) {
+  if (!c->pending || !c->has_graph) return;
+  const uint64_t n = c->nv;
+  if (n) {
+    prepare_chain_layout(c);
+    RNNDG_LAUNCH(c, k_mark_pending, grid_for(n, kBlock), kBlock, 0, n, c->off.p, c->cnt.p,
+                 c->key.p, c->mat_b.ensure(n), c->mat_e.ensure(n));
+    resolve_pending(c);
+  }
+  c->pending = false;
+}
+
 void op_sort_lists(rnndg_ctx* c) {
+  materialize_pending(c);
   const uint64_t n = c->nv;
   ensure_scratch(c);
   RNNDG_LAUNCH(c, k_seg_end, grid_for(n, 256), 256, 0, n, c->off.p, c->cnt.p, nullptr, 0u,
@@ -1233,6 +1341,7 @@ void op_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end) {
   c->nv = v_end - v_begin;
   c->partitioned = true;
   c->has_graph = false;
+  c->pending = false;
 }
 
 uint64_t records_staged(rnndg_ctx* c) {
@@ -1268,6 +1377,7 @@ uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial) {
 
 // stage reverse proposals (kind 1) or in-edges (kind 2) of the owned lists
 uint64_t op_shard_stage(rnndg_ctx* c, int kind) {
+  materialize_pending(c);
   uint64_t m = 0;
   {
     std::vector<uint32_t> cnt(c->nv);
@@ -1371,8 +1481,10 @@ uint64_t op_shard_import(rnndg_ctx* c, int kind, const uint32_t* dst_dev, const 
   const uint32_t* post = kind == RNNDG_X_PENDING ? c->post_cnt.p : c->cnt.p;
   RNNDG_LAUNCH(c, k_apply_count, warp_grid(c, n), kBlock, 0, n, c->off.p, c->key.p, post,
                c->boff.p, c->bkey_s.p, c->bflag.p, c->brank.p, c->cnt_b.p, ctr,
-               kind == RNNDG_X_PENDING ? 1 : 0, int(c->exact_dists));
+               kind == RNNDG_X_PENDING ? 1 : 0,
+               int((kind == RNNDG_X_PENDING && gram_cap()) || !c->exact_dists));
   merge_and_swap(c, post);
+  if (kind == RNNDG_X_PENDING && gram_cap()) c->pending = true;
   if (partial) {
     unsigned long long h[kNumCounters];
     RNNDG_CUDA(cudaMemcpyAsync(h, ctr, sizeof(h), cudaMemcpyDeviceToHost, c->stream));
@@ -1668,6 +1780,7 @@ void op_nnd_finalize(rnndg_ctx* c) {
   RNNDG_LAUNCH(c, k_nd_finalize, warp_grid(c, n), kBlock, 0, n, c->nd_stride, K, c->nd_pool.p,
                c->nd_pcnt.p, c->off.p, c->cnt.p, c->key.p);
   c->has_graph = true;
+  c->pending = false;
   c->has_distances = true;
   c->exact_dists = true;
   RNNDG_CUDA(cudaStreamSynchronize(c->stream));

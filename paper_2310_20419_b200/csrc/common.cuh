@@ -17,6 +17,11 @@ namespace rnndg {
 // ids are unique within a list, so the flag bit never decides an order.
 // 8 bytes per entry instead of the reference's 12-byte NeighborEntry.
 constexpr uint64_t kTomb = ~0ull;  // deleted slot marker (sorts last)
+// "distance pending": a redirected entry whose exact distance is not computed
+// at redirect time (gram.cu computes it while streaming the row at the next
+// scan of the list; materialize_pending() everywhere else).  The bits are a
+// NaN above +inf, so pending entries sort after every real one, by id.
+constexpr uint32_t kPendBits = 0x7F800001u;
 constexpr uint32_t kNone = 0xFFFFFFFFu;
 
 __host__ __device__ __forceinline__ uint64_t make_key(float dist, uint32_t id,
@@ -28,6 +33,12 @@ __host__ __device__ __forceinline__ uint64_t make_key(float dist, uint32_t id,
   __builtin_memcpy(&db, &dist, 4);
 #endif
   return (uint64_t(db) << 32) | (uint64_t(id) << 1) | uint64_t(fresh & 1u);
+}
+__host__ __device__ __forceinline__ uint64_t pending_key(uint32_t id) {
+  return (uint64_t(kPendBits) << 32) | (uint64_t(id) << 1) | 1ull;
+}
+__host__ __device__ __forceinline__ bool key_pending(uint64_t k) {
+  return uint32_t(k >> 32) == kPendBits;
 }
 __host__ __device__ __forceinline__ uint32_t key_id(uint64_t k) {
   return uint32_t(k) >> 1;

@@ -78,6 +78,12 @@ enum Counter : int {
   kEvalHub,    // ... of which by the hub-list kernel
   kBigCount,   // hub lists longer than big_hub_threshold() (cluster-cooperative)
   kLongShortCount,  // short lists longer than long_short_threshold() (queued first)
+  kGram0,      // lists of <= 16 / 32 / 64 / 128 entries queued for the Gram-filtered
+  kGram1,      //   walk (gram.cu), one counter per size class
+  kGram2,
+  kGram3,
+  kGramAmb,    // Gram-filter comparisons inside the error band (decided exactly)
+  kGramExact,  // exact distances evaluated by the Gram-filtered walk
   kNumCounters
 };
 
@@ -115,6 +121,9 @@ struct rnndg_ctx {
   // every cached dist is the exact l2 of its endpoints (true for graphs built
   // here; false after rnndg_set_graph with caller-provided distances)
   bool exact_dists = true;
+  // some list may hold redirected entries whose distance is pending
+  // (common.cuh kPendBits); materialize_pending() resolves them
+  bool pending = false;
 
   // pass scratch
   rnndg::DevBuf<uint8_t> active, touch, bflag;
@@ -141,6 +150,9 @@ struct rnndg_ctx {
   rnndg::DevBuf<float> ex_dists;
   rnndg::DevBuf<uint8_t> ex_fresh;
   rnndg::DevBuf<uint32_t> kpos_g;  // scan scratch for lists > kScanUcap
+  rnndg::DevBuf<uint32_t> gram_q;  // Gram-walk queues, 4 size classes x nv
+  rnndg::DevBuf<uint64_t> mat_b, mat_e;  // lists whose pending distances are resolved
+  rnndg::DevBuf<unsigned long long> gram_prof;  // RNNDG_TRACE cycle counters (gram.cu)
   // sharding: staged (dst, key) records, per-part counts
   rnndg::DevBuf<uint32_t> rec_dst, rec_dst2;
   rnndg::DevBuf<uint64_t> rec_key, rec_key2, part_bounds;
@@ -173,7 +185,7 @@ struct rnndg_ctx {
   uint64_t shard_touched = 0, shard_active = 0, shard_passes = 0;
   // timing events
   cudaEvent_t ev[8] = {};
-  cudaEvent_t ev_scan[2] = {};  // trace only: hub kernel end (side), short kernel end (main)
+  cudaEvent_t ev_scan[3] = {};  // trace only: hub kernel end (side), short kernel end (main), Gram kernel end (main)
 };
 
 namespace rnndg {
@@ -197,6 +209,8 @@ void op_read_counters(rnndg_ctx* c, rnndg_counts* out, double* t_scan, double* t
                       double* t_apply, uint64_t* touched, uint64_t* active_entries);
 void op_reverse(rnndg_ctx* c, uint32_t R, int order);
 void op_sort_lists(rnndg_ctx* c);
+// exact distances for pending entries (all lists), lists re-sorted
+void materialize_pending(rnndg_ctx* c);
 void op_set_partition(rnndg_ctx* c, uint64_t v_begin, uint64_t v_end);
 uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial);
 // NN-Descent baseline (nndescent.cpp, canonical deferred join)

@@ -344,6 +344,7 @@ void op_search(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t L,
                uint32_t K, uint32_t k, int entry_mode, uint32_t entry_vertex,
                uint32_t entry_count, uint64_t seed, uint32_t* ids, float* dists,
                uint64_t* visited, uint64_t* dist_comps) {
+  materialize_pending(c);
   const uint64_t n = c->n;
   if (nq == 0) throw ParamError("batch_search: no queries");
   if (n == 0) throw ParamError("search: empty graph");

@@ -33,8 +33,6 @@
 //                              of a cluster (longest first), the rest by one
 //   k_scan_spec<32, true, 4>   hub lists, one 1024-thread CTA each (rows
 //                              shorter than 2 KB, or RNNDG_HUB=0)
-//   k_scan_block               the same walk with two steps per round
-//                              (RNNDG_SPEC=0)
 // Variants measured slower and removed (smem-staged rows, TMA-sliced rows, a
 // pull walk, a warp-specialised double-buffered kernel, fused multi-distance
 // tasks, early exit, deeper register pipelines): profiles/README.md.
@@ -46,6 +44,7 @@
 #include "common.cuh"
 #include "ctx.hpp"
 #include "scan.cuh"
+#include "quad.cuh"
 
 namespace rnndg {
 
@@ -85,102 +84,6 @@ __global__ void k_chain_layout(const float* __restrict__ x, uint64_t n, uint32_t
   }
 }
 
-// 256-bit read-only loads of chain-blocked blocks.  ld256: the streamed
-// row of a pair (the candidate), L1::no_allocate so it does not evict the
-// rows that are re-read; ld256w: the row shared by many pairs (a provisional
-// kept entry), normal L1 allocation.  C3 1M: 2.25 s -> 2.18 s per build
-// (both rows no_allocate 2.20 s, w rows evict_last 2.18 s).  Short rows
-// (C2 d = 128, C4 d = 96) stay in L1 across rounds: there the streamed row
-// is allocated too (kNA = false; C4 1M 0.97 -> 0.93 s, C2 0.79 -> 0.77 s).
-template <bool kNA = true>
-__device__ __forceinline__ void ld256(const float* p, float (&r)[8]) {
-  if (kNA)
-    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
-                   "=f"(r[6]), "=f"(r[7])
-                 : "l"(p));
-  else
-    asm volatile("ld.global.nc.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
-                   "=f"(r[6]), "=f"(r[7])
-                 : "l"(p));
-}
-__device__ __forceinline__ void ld256w(const float* p, float (&r)[8]) {
-  asm volatile("ld.global.nc.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-               : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
-                 "=f"(r[6]), "=f"(r[7])
-               : "l"(p));
-}
-
-__device__ __forceinline__ void prefetch_row_l2(const float* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
-
-__device__ __forceinline__ void chain_step(const float (&va)[8], const float (&vb)[8], float& s) {
-#pragma unroll
-  for (int i = 0; i < 8; ++i) {
-    const float t = __fsub_rn(va[i], vb[i]);
-    s = __fadd_rn(s, __fmul_rn(t, t));
-  }
-}
-
-// A quad computes d(a, b) on chain-blocked rows, lane k = chain k; the exact
-// total is returned in the quad's chain-0 lane.  All 32 lanes must call.
-// `a` is the streamed row, `b` the row shared across pairs (l2 is
-// bit-symmetric, so the order of the operands never changes a result).
-// Loads run two blocks ahead of the arithmetic.
-template <bool kNA = true>
-__device__ __forceinline__ float quad_l2(const float* __restrict__ a, const float* __restrict__ b,
-                                         uint32_t k, uint32_t nblk, uint32_t ntail) {
-  float s = 0.f;
-  const float* pa = a + 8 * k;
-  const float* pb = b + 8 * k;
-  float a0[8], b0[8], a1[8], b1[8];
-  uint32_t blk = 0;
-  if (nblk >= 2) {
-    ld256<kNA>(pa, a0);
-    ld256w(pb, b0);
-    ld256<kNA>(pa + 32, a1);
-    ld256w(pb + 32, b1);
-    for (blk = 2; blk + 1 < nblk; blk += 2) {
-      chain_step(a0, b0, s);
-      ld256<kNA>(pa + 32 * blk, a0);
-      ld256w(pb + 32 * blk, b0);
-      chain_step(a1, b1, s);
-      ld256<kNA>(pa + 32 * (blk + 1), a1);
-      ld256w(pb + 32 * (blk + 1), b1);
-    }
-    chain_step(a0, b0, s);
-    chain_step(a1, b1, s);
-  }
-  for (; blk < nblk; ++blk) {
-    ld256<kNA>(pa + 32 * blk, a0);
-    ld256w(pb + 32 * blk, b0);
-    chain_step(a0, b0, s);
-  }
-  const float s_next = __shfl_down_sync(0xffffffffu, s, 1);
-  const float pair = __fadd_rn(s, s_next);                    // s0+s1 | s2+s3
-  const float pair2 = __shfl_down_sync(0xffffffffu, pair, 2);
-  float sum = __fadd_rn(pair, pair2);                         // chain-0 lane
-  if (ntail && k == 0) {
-    const float* ta = a + 32 * nblk;
-    const float* tb = b + 32 * nblk;
-    for (uint32_t t = 0; t < ntail; ++t) {
-      const float df = __fsub_rn(__ldg(ta + t), __ldg(tb + t));
-      sum = __fadd_rn(sum, __fmul_rn(df, df));
-    }
-  }
-  return sum;
-}
-
-struct Row {
-  const float* xp;
-  uint32_t stride, nblk, ntail;
-  __device__ const float* operator()(uint64_t key) const {
-    return xp + uint64_t(key_id(key)) * stride;
-  }
-};
-
 struct ScanArgs {
   const uint64_t* act_small;  // short active lists, locality order (low 32 bits = vertex)
   const int* nsmall;
@@ -204,6 +107,7 @@ struct ScanArgs {
   int run_max;   // longest leading run of old entries kept in one round (0: off)
   int run_tasks; // task budget of an old-run round per 64 threads
   int run_min;   // shortest run taken as an old-run round (0: D + 1)
+  int pend;      // redirect records with pending distances (the Gram walk is on)
 };
 
 __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned long long removed,
@@ -245,173 +149,6 @@ __device__ __forceinline__ uint32_t block_rank(bool pred, uint32_t* wcnt, uint32
   return before + __popc(m & ((1u << lane) - 1u));
 }
 
-// One CTA of W warps scans one vertex at a time (persistent, dynamic queue).
-// A push step walks the alive candidates in batches of 32*W: the needed pairs
-// of a batch are compacted into a task list and evaluated 8*W at a time (a
-// quad per pair, a lane per chain), so a step with up to 8*W needed pairs
-// costs one distance latency.  kLong: lists longer than kScanUcap, whose keys
-// and alive list stay in global memory (queue act_list[n ..), work[1]);
-// otherwise keys and alive list live in shared memory (queue act_small,
-// work[0]).
-template <int W, bool kLong>
-__global__ void __launch_bounds__(32 * W, 1) k_scan_block(ScanArgs g) {
-  constexpr uint32_t NT = 32 * W;
-  constexpr uint32_t kCap = kLong ? 1 : kScanUcap;
-  __shared__ uint64_t keys_sh[kCap];
-  __shared__ uint32_t alive_sh[kCap];
-  __shared__ uint32_t tq[2 * NT];  // task: list position of the candidate
-  __shared__ uint64_t tk[2 * NT];  //       its key
-  __shared__ float tres[2 * NT];   //       its distance to the kept entry
-  __shared__ uint8_t tsel[2 * NT]; //       which kept entry (0: w1, 1: w2)
-  __shared__ uint32_t wcnt[W];
-  __shared__ uint32_t s_a, s_w2kept;
-  const uint32_t tid = threadIdx.x, lane = lane_id(), wid = tid >> 5;
-  const uint32_t quad = lane >> 2, chain = lane & 3;
-  const Row row = g.row;  // local copy (no generic pointers into param space)
-  const uint32_t row_bytes = row.stride * 4u;
-  const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount]) : uint32_t(*g.nsmall);
-  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0;
-
-  for (;;) {
-    if (tid == 0) s_a = atomicAdd(g.work + (kLong ? 1 : 0), 1u);
-    __syncthreads();
-    const uint32_t a = s_a;
-    if (a >= nq) break;
-    const uint32_t u = kLong ? g.act_list[g.n + a] : uint32_t(g.act_small[a]);
-    const uint64_t base = g.off[u];
-    const uint32_t U = g.cnt[u];
-    uint64_t* L = g.keys + base;
-    uint8_t* T = g.touch + base;
-    // kLong: keys are read from L directly; the kept entries of a step are
-    // written to L[nk..] with nk <= p < every alive position
-    const uint64_t* K = kLong ? L : keys_sh;
-    uint32_t* A = kLong ? g.alive_g + base : alive_sh;
-    for (uint32_t j = tid; j < U; j += NT) {
-      const uint64_t k = L[j];
-      if (!kLong) keys_sh[j] = k;
-      A[j] = j;
-      if (g.l2pf) prefetch_row_l2(row(k), row_bytes);
-    }
-    __syncthreads();
-    auto rowp = [&](uint32_t, uint64_t key) -> const float* { return row(key); };
-    uint32_t na = U, nk = 0;
-    while (na) {
-      // Two push steps at once: w1 = first alive candidate (kept: every
-      // earlier kept entry has already been tested against it) and w2 = the
-      // second, provisionally kept.  Pairs with w2 are evaluated
-      // speculatively and counted only for candidates that survive w1, and
-      // only if w2 itself survives w1 -- exactly the reference's pairs.
-      const uint32_t p1 = A[0];
-      const uint64_t wk1 = K[p1];
-      const bool wf1 = key_fresh(wk1);
-      const float* xw1 = rowp(p1, wk1);
-      const bool two = na >= 2;
-      const uint32_t p2 = two ? A[1] : p1;
-      const uint64_t wk2 = K[p2];
-      const bool wf2 = key_fresh(wk2);
-      const float* xw2 = rowp(p2, wk2);
-      __syncthreads();  // all threads have read A[0..1] / K[p]
-      if (tid == 0) L[nk] = wk1 & ~1ull;  // flagged old (builder.cpp:68)
-      ++nk;
-      uint32_t nn = 0;  // survivors so far, compacted in place into A[0 ..)
-      bool w2kept = false;
-      for (uint32_t b0 = 1; b0 < na; b0 += NT) {
-        const uint32_t ai = b0 + tid;
-        const bool valid = ai < na;
-        const uint32_t q = valid ? A[ai] : 0u;
-        const uint64_t vk = valid ? K[q] : 0ull;
-        const bool vf = key_fresh(vk);
-        const bool need1 = valid && (wf1 || vf);  // builder.cpp:53-56
-        const bool need2 = valid && ai >= 2 && (wf2 || vf);
-        uint32_t n1, n2;
-        const uint32_t t1 = block_rank<W>(need1, wcnt, n1);
-        const uint32_t t2 = n1 + block_rank<W>(need2, wcnt, n2);
-        if (need1) {
-          tq[t1] = q;
-          tk[t1] = vk;
-          tsel[t1] = 0;
-        }
-        if (need2) {
-          tq[t2] = q;
-          tk[t2] = vk;
-          tsel[t2] = 1;
-        }
-        const uint32_t ntask = n1 + n2;
-        __syncthreads();
-        for (uint32_t t0 = 0; t0 < ntask; t0 += 8 * W) {
-          const uint32_t tw = t0 + 8 * wid;
-          if (tw >= ntask) continue;  // warp-uniform
-          const uint32_t ti = tw + quad;
-          const bool has = ti < ntask;
-          const uint32_t ts = has ? ti : tw;
-          const float* xv = rowp(tq[ts], tk[ts]);
-          const float* xw = tsel[ts] ? xw2 : xw1;
-          const float dist = quad_l2(xv, xw, chain, row.nblk, row.ntail);
-          if (has && chain == 0) tres[ti] = dist;
-        }
-        __syncthreads();
-        // resolve w1 for every candidate; the fate of w2 (candidate ai == 1)
-        // is known in the first batch
-        bool gone = false, by2 = false;
-        float dvw = 0.f;
-        if (need1) {
-          dvw = tres[t1];
-          ++checks;
-          T[q] = 1;
-          T[p1] = 1;
-          gone = key_dist(vk) >= dvw;
-        } else if (valid) {
-          ++skips;
-        }
-        if (ai == 1) s_w2kept = (valid && !gone) ? 1u : 0u;
-        __syncthreads();
-        w2kept = two && s_w2kept;
-        if (valid && !gone && ai >= 2 && w2kept) {
-          if (need2) {
-            const float d2 = tres[t2];
-            ++checks;
-            T[q] = 1;
-            T[p2] = 1;
-            if (key_dist(vk) >= d2) {
-              gone = true;
-              by2 = true;
-              dvw = d2;
-            }
-          } else {
-            ++skips;
-          }
-        }
-        if (gone) {
-          ++removed;
-          const uint32_t w_id = key_id(by2 ? wk2 : wk1);
-          g.pend_src[base + q] = w_id;
-          g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
-          if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
-        }
-        // survivors stay alive; a kept w2 leaves the alive list
-        const bool stay = valid && !gone && !(ai == 1 && w2kept);
-        uint32_t nstay;
-        const uint32_t r = block_rank<W>(stay, wcnt, nstay);
-        // every thread of the batch has read its A[ai] (block_rank syncs)
-        if (stay) A[nn + r] = q;
-        nn += nstay;
-        __syncthreads();
-      }
-      if (w2kept) {
-        if (tid == 0) L[nk] = wk2 & ~1ull;
-        ++nk;
-      }
-      na = nn;
-    }
-    if (tid == 0) g.post_cnt[u] = nk;
-    for (uint32_t j = tid; j < U; j += NT) touched += T[j];
-    __syncthreads();
-  }
-  flush_counters(g.ctr, removed, checks, skips, touched);
-}
-
-// ------------------------------------------------------------ speculative
-// Order-preserving block-wide exclusive scan of per-thread counts c.
 template <int W, bool kTrail = true>
 __device__ __forceinline__ uint32_t block_excl_scan(uint32_t c, uint32_t* wcnt,
                                                     uint32_t& total) {
@@ -436,7 +173,7 @@ __device__ __forceinline__ uint32_t block_excl_scan(uint32_t c, uint32_t* wcnt,
   return before + x - c;
 }
 
-// k_scan_block with D push steps per round.  The first D alive candidates
+// The push walk with D steps per round.  The first D alive candidates
 // w_1..w_D are provisionally kept and every later candidate is evaluated
 // against all of them in the same round (one task per needed pair).  The
 // fates of w_2..w_D are then resolved in list order (w_j is kept iff no kept
@@ -576,7 +313,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
                   ++removed;
                   const uint32_t w_id = key_id(s_rk[i]);
                   g.pend_src[base + q] = w_id;
-                  g.pend_key[base + q] = make_key(d, key_id(vk), 1u);
+                  g.pend_key[base + q] = g.pend ? pending_key(key_id(vk)) : make_key(d, key_id(vk), 1u);
                   if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
                   break;
                 }
@@ -715,7 +452,7 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
             if (by == uint32_t(i)) wkey = wk[i];
           const uint32_t w_id = key_id(wkey);
           g.pend_src[base + q] = w_id;
-          g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
+          g.pend_key[base + q] = g.pend ? pending_key(key_id(vk)) : make_key(dvw, key_id(vk), 1u);
           if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);  // null when sharded
         }
         // survivors stay alive; kept provisional entries leave the alive list
@@ -953,7 +690,7 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
               ++hc.removed;
               const uint32_t w_id = key_id(sm.rk[i]);
               g.pend_src[base + q] = w_id;
-              g.pend_key[base + q] = make_key(d, key_id(vk), 1u);
+              g.pend_key[base + q] = g.pend ? pending_key(key_id(vk)) : make_key(d, key_id(vk), 1u);
               if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
               break;
             }
@@ -1092,7 +829,7 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
               ++hc.removed;
               const uint32_t w_id = key_id(wk[by]);
               g.pend_src[base + wp[j]] = w_id;
-              g.pend_key[base + wp[j]] = make_key(dvw, key_id(wk[j]), 1u);
+              g.pend_key[base + wp[j]] = g.pend ? pending_key(key_id(wk[j])) : make_key(dvw, key_id(wk[j]), 1u);
               if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
             }
           }
@@ -1135,7 +872,7 @@ __device__ __forceinline__ void hub_walk(const ScanArgs& g, uint32_t u, uint32_t
           if (by == uint32_t(i)) wkey = wk[i];
         const uint32_t w_id = key_id(wkey);
         g.pend_src[base + q] = w_id;
-        g.pend_key[base + q] = make_key(dvw, key_id(vk), 1u);
+        g.pend_key[base + q] = g.pend ? pending_key(key_id(vk)) : make_key(dvw, key_id(vk), 1u);
         if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
       }
       const bool stay = valid && !gone;
@@ -1378,15 +1115,15 @@ void prepare_chain_layout(rnndg_ctx* c) {
 }
 
 // provisional kept entries per push round of the short-list kernel:
-// RNNDG_SPEC = 2 | 3 | 4 (default 3) or 0 (k_scan_block, two steps per round,
-// one CTA per hub).  C3 1M before old-run rounds: 2 -> 2.89 s, 3 -> 2.78 s,
+// RNNDG_SPEC = 2 | 3 | 4 (default 3; the two-step k_scan_block it could select
+// in round 1 was removed).  C3 1M before old-run rounds: 2 -> 2.89 s, 3 -> 2.78 s,
 // 4 -> 2.77 s, 6 -> 3.37 s; with them: 2 -> 2.048 s, 3 -> 2.026 s, 4 ->
 // 2.051 s (hub walks keep 4: 3 there costs 2.045 s).
 int spec_mode() {
   static const int v = [] {
     const char* e = std::getenv("RNNDG_SPEC");
     const int x = e ? std::atoi(e) : kShortSpec;
-    return x == 0 || x == 2 || x == 3 || x == 4 ? x : kShortSpec;
+    return x == 2 || x == 3 || x == 4 ? x : kShortSpec;
   }();
   return v;
 }
@@ -1430,7 +1167,8 @@ int hub_cluster_for_pass(rnndg_ctx* c, int mode) {
 }
 
 // Launches both scan kernels; the long-list kernel runs on the side stream
-// and is joined back before returning.  work[0] / work[1] are the queues,
+// and is joined back before returning.  work[0] / work[1] are the queues
+// (work[4] the hub kernel's second queue, work[6] the Gram tiles),
 // work[2] the number of short active lists.
 void launch_scan(rnndg_ctx* c, unsigned int* work) {
   const ScanConfig cfg = scan_config(c);
@@ -1489,6 +1227,7 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     return v < 0 ? 0 : v;
   }();
   a.run_min = run_min;
+  a.pend = gram_cap() ? 1 : 0;
   // two-warp CTAs for short lists (4-warp CTAs measured slower,
   // profiles/README.md)
   constexpr int short_w = kPushWarps;
@@ -1504,7 +1243,6 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     kshort = na ? k_scan_spec<short_w, false, 4, true> : k_scan_spec<short_w, false, 4, false>;
   if (spec == 2)
     kshort = na ? k_scan_spec<short_w, false, 2, true> : k_scan_spec<short_w, false, 2, false>;
-  if (spec == 0) kshort = k_scan_block<short_w, false>;
   const unsigned threads_short = 32u * unsigned(short_w);
   const size_t smem = 0;
   int per_sm = 0;
@@ -1597,9 +1335,7 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     k_sort_big<<<1, 1024, 0, c->side>>>(c->act_list.p, c->nv, c->cnt.p, c->counters.p);
     ++c->launches;
     RNNDG_CUDA(cudaLaunchKernelEx(&cfg, khub, a));
-  } else if (spec == 0)
-    k_scan_block<kLongWarps, true><<<long_grid, 32 * kLongWarps, 0, c->side>>>(a);
-  else if (long_w == 8)
+  } else if (long_w == 8)
     k_scan_spec<8, true, kSpec><<<long_grid, 32 * 8, 0, c->side>>>(a);
   else if (long_w == 16)
     k_scan_spec<16, true, kSpec><<<long_grid, 32 * 16, 0, c->side>>>(a);
@@ -1608,6 +1344,10 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   ++c->launches;
   RNNDG_CUDA(cudaGetLastError());
   if (c->trace) RNNDG_CUDA(cudaEventRecord(c->ev_scan[0], c->side));
+  if (gram_cap()) {
+    launch_gram(c, work);
+    if (c->trace) RNNDG_CUDA(cudaEventRecord(c->ev_scan[2], c->stream));
+  }
   RNNDG_LAUNCH(c, kshort, grid, threads_short, smem, a);
   if (c->trace) RNNDG_CUDA(cudaEventRecord(c->ev_scan[1], c->stream));
   RNNDG_CUDA(cudaEventRecord(c->ev_join, c->side));

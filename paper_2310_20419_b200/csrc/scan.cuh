@@ -23,6 +23,11 @@ struct ScanConfig {
 ScanConfig scan_config(rnndg_ctx* c);
 void prepare_chain_layout(rnndg_ctx* c);
 void launch_scan(rnndg_ctx* c, unsigned int* work);
+// Gram-filtered walk for lists of at most gram_cap() entries (gram.cu;
+// RNNDG_GRAM, 0 = off): k_mark_active queues them by size class
+uint32_t gram_cap();
+void launch_gram(rnndg_ctx* c, unsigned int* work);
+void gram_trace(rnndg_ctx* c);
 // provisional entries per push round (RNNDG_SPEC) and the hub-cluster size
 // (0 = one CTA per hub list); build.cu queues big hubs only when clustered
 int spec_mode();

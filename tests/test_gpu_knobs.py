@@ -1,0 +1,43 @@
+"""Every schedule knob that is kept gives the oracle's graph
+and counters bit for bit: the Gram-filtered walk on / off / capped, the
+short-list kernel's provisional depth, old-run rounds, list orders, the CUB
+sort, the one-CTA-per-hub widths.  Each setting runs tests/knob_case.py in
+its own process (the knobs are read once per process)."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+KNOBS = [
+    {},
+    {"RNNDG_GRAM": "128"},
+    {"RNNDG_GRAM": "32"},
+    {"RNNDG_GRAM": "64"},
+    {"RNNDG_SPEC": "2"},
+    {"RNNDG_SPEC": "4"},
+    {"RNNDG_RUN": "0"},
+    {"RNNDG_ORDER": "1"},
+    {"RNNDG_ORDER": "2"},
+    {"RNNDG_CUBSORT": "1"},
+    {"RNNDG_HUB": "0", "RNNDG_LONG_W": "8"},
+    {"RNNDG_HUB": "0", "RNNDG_LONG_W": "16"},
+    {"RNNDG_UCAP": "128", "RNNDG_LS": "0"},
+]
+
+
+def _id(env):
+    return ",".join(f"{k[6:]}={v}" for k, v in env.items()) or "default"
+
+
+@pytest.mark.parametrize("case", ["passes", "build"])
+@pytest.mark.parametrize("env", KNOBS, ids=_id)
+def test_knob_matches_oracle(env, case):
+    full = dict(os.environ, **env)
+    r = subprocess.run([sys.executable, os.path.join(HERE, "knob_case.py"), case], env=full,
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
