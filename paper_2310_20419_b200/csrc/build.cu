@@ -152,12 +152,13 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
       act = __any_sync(0xffffffffu, j < U && key_fresh(key[b + j]));
     }
     if (lane != 0) continue;
-    if (mat_b) {
+    if (mat_b && act && U > gcap && key_pending(key[b + U - 1])) {
       // an active list the Gram walk does not take, ending in pending
-      // entries (they sort last): its distances are resolved before the scan
-      const bool need = act && U > gcap && U && key_pending(key[b + U - 1]);
-      mat_b[u] = need ? b : 0;
-      mat_e[u] = need ? b + U : 0;
+      // entries (they sort last): queued for resolve_pending before the scan
+      const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kMatCount]), 1u);
+      mat_b[x] = b;
+      mat_e[x] = b + U;
+      mat_e[n + x] = u;  // the list's vertex
     }
     uint8_t flag = 0;
     if (act) {
@@ -699,11 +700,13 @@ __global__ void __launch_bounds__(kBlock) k_seg_sort_warp(const uint64_t* __rest
                                                          uint64_t nseg,
                                                          const uint64_t* __restrict__ begin,
                                                          const uint64_t* __restrict__ end,
-                                                         uint32_t* __restrict__ big) {
+                                                         uint32_t* __restrict__ big,
+                                                         const unsigned long long* nseg_dev) {
   __shared__ uint64_t sh[kWarpsPerBlock][kSegWarpCap];
   const uint32_t lane = lane_id(), wib = threadIdx.x >> 5;
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
+  if (nseg_dev && *nseg_dev < nseg) nseg = *nseg_dev;  // segments counted on the device
   for (uint64_t s = warp; s < nseg; s += nwarps) {
     const uint64_t b = begin[s];
     const uint32_t len = uint32_t(end[s] - b);
@@ -764,7 +767,8 @@ __global__ void __launch_bounds__(1024) k_seg_sort_block(const uint64_t* __restr
 }
 
 void seg_sort_keys(rnndg_ctx* c, const uint64_t* keys_in, uint64_t* keys_out, uint64_t span,
-                   uint64_t nseg, const uint64_t* begin, const uint64_t* end) {
+                   uint64_t nseg, const uint64_t* begin, const uint64_t* end,
+                   const unsigned long long* nseg_dev = nullptr) {
   if (span == 0 || nseg == 0) return;
   static const bool use_cub = [] {
     const char* e = std::getenv("RNNDG_CUBSORT");
@@ -773,11 +777,18 @@ void seg_sort_keys(rnndg_ctx* c, const uint64_t* keys_in, uint64_t* keys_out, ui
   if (!use_cub) {
     uint32_t* big = c->seg_big.ensure(nseg + 1);
     RNNDG_CUDA(cudaMemsetAsync(big, 0, sizeof(uint32_t), c->stream));
-    RNNDG_LAUNCH(c, k_seg_sort_warp, warp_grid(c, nseg), kBlock, 0, keys_in, keys_out, nseg,
-                 begin, end, big);
+    RNNDG_LAUNCH(c, k_seg_sort_warp, nseg_dev ? unsigned(sm_count(c)) * 8u : warp_grid(c, nseg),
+                 kBlock, 0, keys_in, keys_out, nseg, begin, end, big, nseg_dev);
     RNNDG_LAUNCH(c, k_seg_sort_block, unsigned(sm_count(c)), 1024, 0, keys_in, keys_out, begin,
                  end, big);
     return;
+  }
+  if (nseg_dev) {  // CUB needs the count on the host
+    unsigned long long h = 0;
+    RNNDG_CUDA(cudaMemcpyAsync(&h, nseg_dev, 8, cudaMemcpyDeviceToHost, c->stream));
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+    nseg = std::min<uint64_t>(nseg, h);
+    if (nseg == 0) return;
   }
   if (span > uint64_t(INT32_MAX)) throw CudaError("segmented sort span exceeds 2^31");
   size_t bytes = 0;
@@ -1016,25 +1027,29 @@ void op_random_init(rnndg_ctx* c, uint32_t S, uint64_t seed) {
 __global__ void __launch_bounds__(kBlock)
     k_mark_pending(uint64_t n, const uint64_t* __restrict__ off, const uint32_t* __restrict__ cnt,
                    const uint64_t* __restrict__ key, uint64_t* __restrict__ mat_b,
-                   uint64_t* __restrict__ mat_e) {
+                   uint64_t* __restrict__ mat_e, unsigned long long* __restrict__ count) {
   for (uint64_t u = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; u < n;
        u += uint64_t(gridDim.x) * blockDim.x) {
     const uint64_t b = off[u];
     const uint32_t U = cnt[u];
-    const bool need = U && key_pending(key[b + U - 1]);
-    mat_b[u] = need ? b : 0;
-    mat_e[u] = need ? b + U : 0;
+    if (U && key_pending(key[b + U - 1])) {
+      const unsigned long long x = atomicAdd(count, 1ull);
+      mat_b[x] = b;
+      mat_e[x] = b + U;
+      mat_e[n + x] = u;
+    }
   }
 }
 
 __global__ void __launch_bounds__(kBlock)
     k_resolve_pending(uint64_t n, uint64_t v0, const uint64_t* __restrict__ mat_b,
-                      const uint64_t* __restrict__ mat_e, uint64_t* __restrict__ key, Row row) {
+                      const uint64_t* __restrict__ mat_e, const unsigned long long* __restrict__ count,
+                      uint64_t* __restrict__ key, Row row) {
   __shared__ uint32_t q[kWarpsPerBlock][32];
   const uint32_t lane = lane_id(), wib = threadIdx.x >> 5, quad = lane >> 2, chain = lane & 3;
-  WARP_LOOP(u, n) {
-    const uint64_t b = mat_b[u], e = mat_e[u];
-    if (b == e) continue;
+  const uint64_t nq = *count;
+  WARP_LOOP(x, nq) {
+    const uint64_t b = mat_b[x], e = mat_e[x], u = mat_e[n + x];
     const float* xu = row.xp + (v0 + u) * row.stride;
     for (uint64_t j0 = b; j0 < e; j0 += 32) {
       const bool pend = j0 + lane < e && key_pending(key[j0 + lane]);
@@ -1056,7 +1071,7 @@ __global__ void __launch_bounds__(kBlock)
 }
 
 namespace {
-void resolve_pending(rnndg_ctx* c);
+void resolve_pending(rnndg_ctx* c, const unsigned long long* count);
 }  // namespace
 
 // Scan phase of a pass: counters zeroed, active vertices marked, locality
@@ -1076,10 +1091,11 @@ void op_scan_phase(rnndg_ctx* c) {
     RNNDG_LAUNCH(c, k_mark_active, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
                  big_hub_threshold(c), long_short_threshold(), gram_cap(), c->gram_q.p,
-                 c->pending ? c->mat_b.ensure(n) : nullptr, c->pending ? c->mat_e.ensure(n) : nullptr);
+                 c->pending ? c->mat_b.ensure(n) : nullptr,
+                 c->pending ? c->mat_e.ensure(2 * n) : nullptr);
   if (c->pending && n) {
     prepare_chain_layout(c);
-    resolve_pending(c);
+    resolve_pending(c, c->counters.p + kMatCount);
   }
   locality_order(c);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
@@ -1303,12 +1319,12 @@ void op_reverse(rnndg_ctx* c, uint32_t R, int order) {
 namespace {
 // exact distances of the pending entries of the lists marked in mat_b /
 // mat_e, then those lists re-sorted in place
-void resolve_pending(rnndg_ctx* c) {
+void resolve_pending(rnndg_ctx* c, const unsigned long long* count) {
   const uint64_t n = c->nv;
   const ScanConfig cfg = scan_config(c);
-  RNNDG_LAUNCH(c, k_resolve_pending, warp_grid(c, n), kBlock, 0, n, c->v0, c->mat_b.p,
-               c->mat_e.p, c->key.p, Row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail});
-  seg_sort_keys(c, c->key.p, c->key.p, c->span, n, c->mat_b.p, c->mat_e.p);
+  RNNDG_LAUNCH(c, k_resolve_pending, unsigned(sm_count(c)) * 8u, kBlock, 0, n, c->v0, c->mat_b.p,
+               c->mat_e.p, count, c->key.p, Row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail});
+  seg_sort_keys(c, c->key.p, c->key.p, c->span, n, c->mat_b.p, c->mat_e.p, count);
 }
 }  // namespace
 
@@ -1317,9 +1333,11 @@ void materialize_pending(rnndg_ctx* c) {
   const uint64_t n = c->nv;
   if (n) {
     prepare_chain_layout(c);
+    unsigned long long* count = c->counters.p + kMatCount;
+    zero(c, count, 1);
     RNNDG_LAUNCH(c, k_mark_pending, grid_for(n, kBlock), kBlock, 0, n, c->off.p, c->cnt.p,
-                 c->key.p, c->mat_b.ensure(n), c->mat_e.ensure(n));
-    resolve_pending(c);
+                 c->key.p, c->mat_b.ensure(n), c->mat_e.ensure(2 * n), count);
+    resolve_pending(c, count);
   }
   c->pending = false;
 }

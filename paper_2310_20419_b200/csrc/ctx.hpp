@@ -84,6 +84,7 @@ enum Counter : int {
   kGram3,
   kGramAmb,    // Gram-filter comparisons inside the error band (decided exactly)
   kGramExact,  // exact distances evaluated by the Gram-filtered walk
+  kMatCount,   // lists queued for resolve_pending (build.cu)
   kNumCounters
 };
 
@@ -151,7 +152,8 @@ struct rnndg_ctx {
   rnndg::DevBuf<uint8_t> ex_fresh;
   rnndg::DevBuf<uint32_t> kpos_g;  // scan scratch for lists > kScanUcap
   rnndg::DevBuf<uint32_t> gram_q;  // Gram-walk queues, 4 size classes x nv
-  rnndg::DevBuf<uint64_t> mat_b, mat_e;  // lists whose pending distances are resolved
+  // lists whose pending distances are resolved: [mat_b[x], mat_e[x]), vertex mat_e[nv + x]
+  rnndg::DevBuf<uint64_t> mat_b, mat_e;
   rnndg::DevBuf<unsigned long long> gram_prof;  // RNNDG_TRACE cycle counters (gram.cu)
   // sharding: staged (dst, key) records, per-part counts
   rnndg::DevBuf<uint32_t> rec_dst, rec_dst2;

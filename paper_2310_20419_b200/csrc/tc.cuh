@@ -22,6 +22,12 @@ __device__ __forceinline__ uint32_t sw128_off(uint32_t r, uint32_t c) {
   return ((r >> 3) << 10) | ((r & 7u) << 7) | (((c ^ r) & 7u) << 4);
 }
 
+// byte offset of 16-byte unit c (0..3) of row r in a 128-row SW64 tile
+// (64 B per row, 8-row atoms of 512 B; unit c sits at c ^ ((r / 2) % 4))
+__device__ __forceinline__ uint32_t sw64_off(uint32_t r, uint32_t c) {
+  return ((r >> 3) << 9) | ((r & 7u) << 6) | (((c ^ (r >> 1)) & 3u) << 4);
+}
+
 // ------------------------------------------------------------- mbarriers
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count)
@@ -50,6 +56,24 @@ __device__ __forceinline__ bool mbar_try_wait(uint64_t* b, uint32_t parity) {
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
   while (!mbar_try_wait(b, parity)) {
   }
+}
+
+// arrive and add `bytes` to the phase's expected transaction count
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile(
+      "{\n\t.reg .b64 st;\n\t"
+      "mbarrier.arrive.expect_tx.release.cta.shared::cta.b64 st, [%0], %1;\n\t}" ::"r"(
+          smem_u32(b)),
+      "r"(bytes)
+      : "memory");
+}
+// bulk global -> shared copy (TMA, no tensor map), completion on an mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
 }
 
 // generic-proxy shared-memory writes -> visible to the tensor core (async proxy)
@@ -89,6 +113,17 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
   d |= uint64_t(1024u >> 4) << 32;    // SBO
   d |= uint64_t(1u) << 46;            // version
   d |= uint64_t(2u) << 61;            // SWIZZLE_128B
+  return d;
+}
+
+// K-major, SWIZZLE_64B: rows of 64 B, 8-row atoms 512 B apart
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= uint64_t((saddr >> 4) & 0x3FFFu);
+  d |= uint64_t(1u) << 16;            // LBO (unused)
+  d |= uint64_t(512u >> 4) << 32;     // SBO
+  d |= uint64_t(1u) << 46;            // version
+  d |= uint64_t(4u) << 61;            // SWIZZLE_64B
   return d;
 }
 
@@ -144,6 +179,28 @@ __device__ __forceinline__ void split2(float a, float b, uint32_t& hi, uint32_t&
   const float ha = __uint_as_float(hi << 16), hb = __uint_as_float(hi & 0xFFFF0000u);
   const float ra = __fsub_rn(a, ha), rb = __fsub_rn(b, hb);
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(lo) : "f"(rb), "f"(ra));
+}
+
+// packed fp32 pairs (FADD2 / FMUL2 on sm_100): each lane IEEE round-to-nearest
+__device__ __forceinline__ uint64_t pk2(float x, float y) {
+  uint64_t v;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "f"(x), "f"(y));
+  return v;
+}
+__device__ __forceinline__ void upk2(uint64_t v, float& x, float& y) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(x), "=f"(y) : "l"(v));
+}
+__device__ __forceinline__ uint64_t sub2(uint64_t a, uint64_t b) {
+  uint64_t r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+// t * t exactly as mul.rn (fma with a -0 addend: one rounding, and ptxas
+// cannot fuse it with a later add)
+__device__ __forceinline__ uint64_t sqr2(uint64_t t) {
+  uint64_t r;
+  asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(r) : "l"(t), "l"(0x8000000080000000ull));
+  return r;
 }
 
 }  // namespace tc

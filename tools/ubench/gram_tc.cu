@@ -14,7 +14,11 @@
 
 using namespace rnndg;
 
-constexpr int kRows = 128, kChunk = 64;
+constexpr int kRows = 128;
+#ifndef CHUNK
+#define CHUNK 64
+#endif
+constexpr int kChunk = CHUNK;  // 64: SWIZZLE_128B rows, 32: SWIZZLE_64B rows
 
 __global__ void __launch_bounds__(128, 1) k_gram(const float* __restrict__ x, const float* __restrict__ u,
                                                  int d, float* __restrict__ g, int reps) {
@@ -40,8 +44,8 @@ __global__ void __launch_bounds__(128, 1) k_gram(const float* __restrict__ x, co
   for (int rep = 0; rep < reps; ++rep) {
     for (int ch = 0; ch < nch; ++ch) {
       // 128 rows x 8 units of 8 elements: 1024 items, 8 per thread
-      for (int it = tid; it < kRows * 8; it += 128) {
-        const int r = it >> 3, c = it & 7;
+      for (int it = tid; it < kRows * (kChunk / 8); it += 128) {
+        const int r = it / (kChunk / 8), c = it % (kChunk / 8);
         float v[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
@@ -51,7 +55,7 @@ __global__ void __launch_bounds__(128, 1) k_gram(const float* __restrict__ x, co
         uint32_t h[4], l[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) tc::split2(v[2 * e], v[2 * e + 1], h[e], l[e]);
-        const uint32_t off = tc::sw128_off(r, c);
+        const uint32_t off = kChunk == 64 ? tc::sw128_off(r, c) : tc::sw64_off(r, c);
         *reinterpret_cast<uint4*>(H + off) = make_uint4(h[0], h[1], h[2], h[3]);
         *reinterpret_cast<uint4*>(L + off) = make_uint4(l[0], l[1], l[2], l[3]);
       }
@@ -62,7 +66,8 @@ __global__ void __launch_bounds__(128, 1) k_gram(const float* __restrict__ x, co
         const uint32_t ha = tc::smem_u32(H), la = tc::smem_u32(L);
 #pragma unroll
         for (int k = 0; k < kChunk / 16; ++k) {
-          const uint64_t dh = tc::sw128_desc(ha + 32 * k), dl = tc::sw128_desc(la + 32 * k);
+          const uint64_t dh = kChunk == 64 ? tc::sw128_desc(ha + 32 * k) : tc::sw64_desc(ha + 32 * k);
+          const uint64_t dl = kChunk == 64 ? tc::sw128_desc(la + 32 * k) : tc::sw64_desc(la + 32 * k);
           const uint32_t acc = (ch | k) ? 1u : 0u;
           tc::mma_bf16(tm, dh, dh, idesc, acc);
           tc::mma_bf16(tm, dh, dl, idesc, 1u);
@@ -147,6 +152,6 @@ int main() {
   cudaEventSynchronize(t1);
   float ms;
   cudaEventElapsedTime(&ms, t0, t1);
-  printf("one CTA, unpipelined: %.2f us per 128x128x960 tile (3 MMA sets)\n", ms * 1e3 / 100);
+  printf("chunk %d: one CTA, unpipelined: %.2f us per 128x128x960 tile (3 MMA sets)\n", kChunk, ms * 1e3 / 100);
   return bad ? 2 : 0;
 }
