@@ -168,7 +168,7 @@ struct rnndg_ctx {
 
   // eval scratch
   rnndg::DevBuf<float> q_dev;
-  rnndg::DevBuf<uint32_t> ids_dev, entry_dev, seen_bits;
+  rnndg::DevBuf<uint32_t> ids_dev, entry_dev, seen_bits, sample_bits;
   rnndg::DevBuf<float> dists_dev;
   rnndg::DevBuf<unsigned long long> qstat_dev;
 

@@ -2,6 +2,7 @@
 // (search.cpp:40-132), exact brute-force ground truth (dataset.cpp:175-205),
 // batched exact L2 (metric.hpp:47-65), rng_strategy (builder.cpp:196-212) and
 // degree statistics (graph.cpp:76-100).
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -17,7 +18,12 @@ namespace {
 // ----------------------------------------------------------------- search
 //
 // One warp per query.  The pool holds up to L (dist, id) keys ascending plus
-// an `expanded` byte per slot; the seen set is a per-block n-bit map.  The
+// an `expanded` byte per slot.  The seen set (search.cpp:46) is an
+// open-addressing hash table of ids sized from L and the degree cap, in
+// global memory per block (L2-resident, cleared per query: O(L * degree),
+// not O(n));
+// a query that fills it past 3/4 stops and is re-run with a per-block n-bit
+// map (kTab = false), so the result never depends on the table size.  The
 // pool after any batch of consider() calls is top-L(pool ∪ new) under
 // (dist, id) (search.cpp:49-59), so a batch of up to 32 neighbours is
 // evaluated in parallel (one lane per neighbour, exact L2) and inserted one
@@ -38,8 +44,10 @@ struct SearchArgs {
   uint32_t entry_vertex;
   const uint32_t* entries;
   uint32_t nentries;
-  uint32_t* seen;       // per block: words_per_map words
+  uint32_t* seen;       // bitmap mode: per block words_per_map words
   uint64_t words_per_map;
+  uint32_t tab_log2;    // hash mode: open-addressing table of 2^tab_log2 ids
+  uint32_t* gtab;       //   per block in global memory (null: in shared memory)
   uint64_t* gpool;      // per block L keys when the pool does not fit smem
   uint8_t* gexp;        // per block L flags
   uint32_t* out_ids;
@@ -48,12 +56,34 @@ struct SearchArgs {
   unsigned long long* out_comps;
 };
 
-template <bool kVec4>
+constexpr uint32_t kTabEmpty = 0xFFFFFFFFu;
+
+// insert id into the seen set; true when it was not there yet
+template <bool kTab>
+__device__ __forceinline__ bool seen_insert(uint32_t* seen, uint32_t tab_log2, uint32_t id) {
+  if (!kTab) {
+    const uint32_t bit = 1u << (id & 31u);
+    return !(atomicOr(&seen[id >> 5], bit) & bit);
+  }
+  const uint32_t mask = (1u << tab_log2) - 1u;
+  uint32_t h = (id * 2654435761u) >> (32u - tab_log2);
+  for (uint32_t probe = 0; probe <= mask; ++probe) {
+    const uint32_t prev = atomicCAS(&seen[h], kTabEmpty, id);
+    if (prev == kTabEmpty) return true;
+    if (prev == id) return false;
+    h = (h + 1u) & mask;
+  }
+  // table full: the query overflows (comps passes 3/4 of the table) and is
+  // re-run with the bitmap, so this answer is never used
+  return true;
+}
+
+template <bool kVec4, bool kTab>
 __device__ void consider_batch(const float* __restrict__ x, uint32_t d, uint32_t L,
                                const float* q,
                                const uint32_t* cand, uint32_t m, uint32_t* seen,
-                               uint64_t* pool, uint8_t* expd, uint32_t& psize,
-                               unsigned long long& comps) {
+                               uint32_t tab_log2, uint64_t* pool, uint8_t* expd,
+                               uint32_t& psize, unsigned long long& comps) {
   const uint32_t lane = lane_id();
   for (uint32_t c0 = 0; c0 < m; c0 += 32) {
     const uint32_t c = c0 + lane;
@@ -61,9 +91,7 @@ __device__ void consider_batch(const float* __restrict__ x, uint32_t d, uint32_t
     uint64_t ck = 0;
     if (c < m) {
       const uint32_t id = cand[c];
-      const uint32_t bit = 1u << (id & 31u);
-      const uint32_t old = atomicOr(&seen[id >> 5], bit);
-      if (!(old & bit)) {
+      if (seen_insert<kTab>(seen, tab_log2, id)) {
         fresh = true;
         const float dist = l2_exact<kVec4>(q, x + uint64_t(id) * d, d);
         ck = (uint64_t(__float_as_uint(dist)) << 32) | id;
@@ -110,24 +138,33 @@ __device__ void consider_batch(const float* __restrict__ x, uint32_t d, uint32_t
   }
 }
 
-template <bool kVec4>
-__global__ void k_search(SearchArgs a) {
+// kTab: hash-table seen set (queries[qi] for qi in `only` when given: the
+// bitmap re-run of the queries that overflowed their table)
+template <bool kVec4, bool kTab>
+__global__ void k_search(SearchArgs a, const uint32_t* only, uint32_t nonly) {
   extern __shared__ __align__(16) unsigned char smem[];
   const uint32_t lane = lane_id();
   float* q = reinterpret_cast<float*>(smem);
   const size_t qbytes = (size_t(a.d) * 4 + 15) & ~size_t(15);
   uint64_t* pool;
   uint8_t* expd;
+  size_t used = qbytes;
   if (a.gpool) {
     pool = a.gpool + uint64_t(blockIdx.x) * a.L;
     expd = a.gexp + uint64_t(blockIdx.x) * a.L;
   } else {
     pool = reinterpret_cast<uint64_t*>(smem + qbytes);
     expd = reinterpret_cast<uint8_t*>(pool + a.L);
+    used += (size_t(a.L) * 9 + 15) & ~size_t(15);
   }
-  uint32_t* seen = a.seen + uint64_t(blockIdx.x) * a.words_per_map;
-  for (uint64_t qi = blockIdx.x; qi < a.nq; qi += gridDim.x) {
-    for (uint64_t w = lane; w < a.words_per_map; w += 32) seen[w] = 0u;
+  const uint64_t seen_words = kTab ? (uint64_t(1) << a.tab_log2) : a.words_per_map;
+  uint32_t* seen = kTab ? (a.gtab ? a.gtab + uint64_t(blockIdx.x) * seen_words
+                                  : reinterpret_cast<uint32_t*>(smem + used))
+                        : a.seen + uint64_t(blockIdx.x) * a.words_per_map;
+  const uint64_t nrun = only ? nonly : a.nq;
+  for (uint64_t qr = blockIdx.x; qr < nrun; qr += gridDim.x) {
+    const uint64_t qi = only ? only[qr] : qr;
+    for (uint64_t w = lane; w < seen_words; w += 32) seen[w] = kTab ? kTabEmpty : 0u;
     for (uint32_t j = lane; j < a.d; j += 32) q[j] = a.queries[qi * a.d + j];
     __syncwarp();
     uint32_t psize = 0;
@@ -136,10 +173,19 @@ __global__ void k_search(SearchArgs a) {
     if (lane == 0) entry_buf[0] = a.entry_vertex;
     __syncwarp();
     if (a.fixed)
-      consider_batch<kVec4>(a.x, a.d, a.L, q, entry_buf, 1, seen, pool, expd, psize, comps);
+      consider_batch<kVec4, kTab>(a.x, a.d, a.L, q, entry_buf, 1, seen, a.tab_log2, pool, expd,
+                                  psize, comps);
     else
-      consider_batch<kVec4>(a.x, a.d, a.L, q, a.entries, a.nentries, seen, pool, expd, psize, comps);
+      consider_batch<kVec4, kTab>(a.x, a.d, a.L, q, a.entries, a.nentries, seen, a.tab_log2, pool,
+                                  expd, psize, comps);
+    bool overflow = false;
     for (;;) {
+      // every considered id is in the seen set: past 3/4 of the table the
+      // query is abandoned and re-run with the bitmap
+      if (kTab && comps > (3ull << a.tab_log2) / 4) {
+        overflow = true;
+        break;
+      }
       uint32_t at = psize;
       for (uint32_t p0 = 0; p0 < psize; p0 += 32) {
         const uint32_t p = p0 + lane;
@@ -170,7 +216,8 @@ __global__ void k_search(SearchArgs a) {
         ids_buf[lane] = id;
         __syncwarp();
         const uint32_t m = take - j0 < 32 ? take - j0 : 32;
-        consider_batch<kVec4>(a.x, a.d, a.L, q, ids_buf, m, seen, pool, expd, psize, comps);
+        consider_batch<kVec4, kTab>(a.x, a.d, a.L, q, ids_buf, m, seen, a.tab_log2, pool, expd,
+                                    psize, comps);
       }
     }
     const uint32_t take = a.k < psize ? a.k : psize;
@@ -181,11 +228,20 @@ __global__ void k_search(SearchArgs a) {
           have ? __uint_as_float(uint32_t(pool[j] >> 32)) : __int_as_float(0x7f800000);
     }
     if (lane == 0) {
-      a.out_visited[qi] = visited;
+      a.out_visited[qi] = overflow ? ~0ull : visited;
       a.out_comps[qi] = comps;
     }
     __syncwarp();
   }
+}
+
+__global__ void k_sum_u32(const uint32_t* __restrict__ v, uint64_t n, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (uint64_t i = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += uint64_t(gridDim.x) * blockDim.x)
+    m += v[i];
+  for (int o = 16; o; o >>= 1) m += __shfl_xor_sync(0xffffffffu, m, o);
+  if (lane_id() == 0 && m) atomicAdd(out, m);
 }
 
 // sample_distinct(SplitMix64(seed), n, count) with no exclusion (rng.hpp:46-72)
@@ -372,24 +428,53 @@ void op_search(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t L,
 
   const uint64_t words = (n + 31) / 32;
   unsigned grid = unsigned(nq < uint64_t(sm_count(c)) * 8 ? nq : uint64_t(sm_count(c)) * 8);
-  uint32_t* scratch = c->seen_bits.ensure(words * (grid + 1));
-  a.seen = scratch;
-  a.words_per_map = words;
   if (!a.fixed) {
     uint32_t count = entry_count ? uint32_t(entry_count < n ? entry_count : n)
                                  : uint32_t(L < n ? L : n);
     uint32_t* ent = c->entry_dev.ensure(count);
     uint32_t* bitmap = nullptr;
-    if (count > 64) {
-      bitmap = scratch + words * grid;
+    if (count > 64) {  // the sampler's membership map (n bits, once per call)
+      bitmap = c->sample_bits.ensure(words);
       RNNDG_CUDA(cudaMemsetAsync(bitmap, 0, words * 4, c->stream));
     }
     RNNDG_LAUNCH(c, k_sample_entries, 1, 32, 0, n, count, seed, ent, bitmap);
     a.entries = ent;
     a.nentries = count;
   }
+  uint32_t* oid = c->ids_dev.ensure(nq * k);
+  float* odist = c->dists_dev.ensure(nq * k);
+  unsigned long long* st = c->qstat_dev.ensure(2 * nq + 1);
+  a.out_ids = oid;
+  a.out_dists = odist;
+  a.out_visited = st;
+  a.out_comps = st + nq;
+  // seen-set table: ~4 x the distances a query is expected to evaluate
+  // (entries + L expansions x the mean out-degree, or K), at least 2^12
+  // ids, per block in global memory (L2-resident; cleared per query).  A
+  // query past 3/4 of it is re-run with the bitmap, so the mean is enough.
+  uint64_t degsum = uint64_t(K) * c->nv;
+  if (!K) {
+    unsigned long long* dm = st + 2 * nq;
+    RNNDG_CUDA(cudaMemsetAsync(dm, 0, 8, c->stream));
+    RNNDG_LAUNCH(c, k_sum_u32, unsigned(sm_count(c)) * 4u, 256, 0, c->cnt.p, c->nv, dm);
+    RNNDG_CUDA(cudaMemcpyAsync(&degsum, dm, 8, cudaMemcpyDeviceToHost, c->stream));
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  }
+  const uint64_t meandeg = c->nv ? (degsum + c->nv - 1) / c->nv : 1;
+  const uint64_t expect = (a.fixed ? 1ull : uint64_t(a.nentries)) + uint64_t(L) * (meandeg + 1);
+  uint32_t lg = 12;
+  while (lg < 26 && (uint64_t(1) << lg) < 4 * expect) ++lg;
+  // RNNDG_SEARCH_TAB: force the table size (tests drive the bitmap re-run)
+  static const int force_lg = [] {
+    const char* e = std::getenv("RNNDG_SEARCH_TAB");
+    return e ? std::atoi(e) : 0;
+  }();
+  if (force_lg >= 4 && force_lg <= 26) lg = uint32_t(force_lg);
+  a.tab_log2 = lg;
+  a.gtab = c->seen_bits.ensure((uint64_t(1) << lg) * grid);
   const size_t qbytes = (size_t(c->d) * 4 + 15) & ~size_t(15);
-  size_t smem = qbytes + size_t(L) * 9;
+  const size_t pbytes = (size_t(L) * 9 + 15) & ~size_t(15);
+  size_t smem = qbytes + pbytes;
   DevBuf<uint64_t> gpool;
   DevBuf<uint8_t> gexp;
   if (smem > 160 * 1024) {
@@ -399,24 +484,48 @@ void op_search(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t L,
     a.gexp = gexp.p;
     smem = qbytes;
   }
-  uint32_t* oid = c->ids_dev.ensure(nq * k);
-  float* odist = c->dists_dev.ensure(nq * k);
-  unsigned long long* st = c->qstat_dev.ensure(2 * nq);
-  a.out_ids = oid;
-  a.out_dists = odist;
-  a.out_visited = st;
-  a.out_comps = st + nq;
-  if (c->d % 4 == 0) {
-    RNNDG_CUDA(cudaFuncSetAttribute(k_search<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    RNNDG_LAUNCH(c, k_search<true>, grid, 32, smem, a);
-  } else {
-    RNNDG_CUDA(cudaFuncSetAttribute(k_search<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    RNNDG_LAUNCH(c, k_search<false>, grid, 32, smem, a);
+  auto launch = [&](auto kern, unsigned g, size_t sm, const uint32_t* only, uint32_t nonly) {
+    // the attribute is raised once per kernel to the largest size used so far
+    static size_t set_for[4] = {0, 0, 0, 0};
+    static const void* fn[4] = {nullptr, nullptr, nullptr, nullptr};
+    int slot = 0;
+    while (slot < 3 && fn[slot] && fn[slot] != reinterpret_cast<const void*>(kern)) ++slot;
+    fn[slot] = reinterpret_cast<const void*>(kern);
+    if (sm > set_for[slot]) {
+      RNNDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sm)));
+      set_for[slot] = sm;
+    }
+    RNNDG_LAUNCH(c, kern, g, 32, sm, a, only, nonly);
+  };
+  if (c->d % 4 == 0)
+    launch(k_search<true, true>, grid, smem, nullptr, 0u);
+  else
+    launch(k_search<false, true>, grid, smem, nullptr, 0u);
+  std::vector<unsigned long long> h(2 * nq);
+  RNNDG_CUDA(cudaMemcpyAsync(h.data(), st, 2 * nq * 8, cudaMemcpyDeviceToHost, c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  // queries that overflowed their table: again with an n-bit map each
+  std::vector<uint32_t> redo;
+  for (uint64_t i = 0; i < nq; ++i)
+    if (h[i] == ~0ull) redo.push_back(uint32_t(i));
+  if (!redo.empty()) {
+    const unsigned g2 = unsigned(redo.size() < 64 ? redo.size() : 64);
+    DevBuf<uint32_t> only, bits;
+    only.ensure(redo.size());
+    RNNDG_CUDA(cudaMemcpyAsync(only.p, redo.data(), redo.size() * 4, cudaMemcpyHostToDevice,
+                               c->stream));
+    a.seen = bits.ensure(words * g2);  // <= 64 blocks x n bits, this call only
+    a.words_per_map = words;
+    const size_t sm2 = a.gpool ? qbytes : qbytes + pbytes;
+    if (c->d % 4 == 0)
+      launch(k_search<true, false>, g2, sm2, only.p, uint32_t(redo.size()));
+    else
+      launch(k_search<false, false>, g2, sm2, only.p, uint32_t(redo.size()));
+    RNNDG_CUDA(cudaMemcpyAsync(h.data(), st, 2 * nq * 8, cudaMemcpyDeviceToHost, c->stream));
+    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
   }
   RNNDG_CUDA(cudaMemcpyAsync(ids, oid, nq * k * 4, cudaMemcpyDeviceToHost, c->stream));
   RNNDG_CUDA(cudaMemcpyAsync(dists, odist, nq * k * 4, cudaMemcpyDeviceToHost, c->stream));
-  std::vector<unsigned long long> h(2 * nq);
-  RNNDG_CUDA(cudaMemcpyAsync(h.data(), st, 2 * nq * 8, cudaMemcpyDeviceToHost, c->stream));
   RNNDG_CUDA(cudaStreamSynchronize(c->stream));
   for (uint64_t i = 0; i < nq; ++i) {
     if (visited) visited[i] = h[i];

@@ -41,3 +41,15 @@ def test_knob_matches_oracle(env, case):
     r = subprocess.run([sys.executable, os.path.join(HERE, "knob_case.py"), case], env=full,
                        capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("tab", ["4", "6"])
+def test_search_bitmap_rerun_matches(tab):
+    """A seen-set table too small for the queries (RNNDG_SEARCH_TAB forces
+    2^4 / 2^6 ids): every query overflows it and is re-run with the n-bit
+    map (eval.cu k_search), so the search parity cases must still pass."""
+    full = dict(os.environ, RNNDG_SEARCH_TAB=tab)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(HERE, "test_gpu_parity.py"), "-k", "search"],
+                       env=full, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
