@@ -12,102 +12,27 @@
 //   builder.hpp:84-86  build              -> rnndg_build
 //
 // `threads` is accepted and ignored: the device always runs the deferred,
-// canonical pass the reference runs for threads > 1 (builder.cpp:88-139).
-// Error codes map back to the reference's exception classes.
+// canonical pass the reference runs for threads > 1 (builder.cpp:88-139);
+// with threads == 1 the reference runs update_serial (:71-86), whose
+// order-dependent redirects give a different graph -- not reproduced here.
+// Error codes map back to the reference's exception classes; the store and
+// graph uploads are cached per thread (rnndg_shim.hpp).
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "rnnd/builder.hpp"
 #include "rnndg.h"
+#include "rnndg_shim.hpp"
 
 namespace rnnd {
 
-namespace {
-
-struct Ctx {
-  rnndg_ctx* h = nullptr;
-  const VectorStore* store = nullptr;
-  const float* data = nullptr;
-  size_t n = 0, d = 0;
-  Ctx() {
-    if (rnndg_create(&h, 0) != RNNDG_OK) throw std::runtime_error("rnndg: no CUDA device");
-  }
-  ~Ctx() { rnndg_destroy(h); }
-};
-
-Ctx& ctx() {
-  thread_local Ctx c;
-  return c;
-}
-
-void check(int rc) {
-  if (rc == RNNDG_OK) return;
-  std::string msg = rnndg_last_error(ctx().h);
-  if (rc == RNNDG_EPARAM) throw ParamError(msg);
-  if (rc == RNNDG_EDATA) throw DataError(msg);
-  throw std::runtime_error(msg);
-}
-
-// The store is uploaded on every call: the caller may mutate or reallocate
-// it between calls (a cached pointer is not an identity).
-void bind_store(const VectorStore& s) {
-  Ctx& c = ctx();
-  check(rnndg_set_data(c.h, s.data.data(), s.n, uint32_t(s.d)));
-  c.store = &s;
-  c.data = s.data.data();
-  c.n = s.n;
-  c.d = s.d;
-}
-
-void upload(const AdjacencyGraph& g) {
-  const size_t n = g.size();
-  std::vector<uint64_t> off(n + 1, 0);
-  for (size_t u = 0; u < n; ++u) off[u + 1] = off[u] + g.adj[u].size();
-  std::vector<uint32_t> ids(off[n]);
-  std::vector<float> dists(off[n]);
-  std::vector<uint8_t> fresh(off[n]);
-  for (size_t u = 0; u < n; ++u)
-    for (size_t j = 0; j < g.adj[u].size(); ++j) {
-      const auto& e = g.adj[u][j];
-      ids[off[u] + j] = e.id;
-      dists[off[u] + j] = e.dist;
-      fresh[off[u] + j] = e.fresh ? 1 : 0;
-    }
-  check(rnndg_set_graph(ctx().h, n, off.data(), ids.data(), dists.data(), fresh.data()));
-}
-
-void download(AdjacencyGraph& g) {
-  uint64_t n = 0, m = 0;
-  check(rnndg_graph_size(ctx().h, &n, &m));
-  std::vector<uint64_t> off(n + 1);
-  std::vector<uint32_t> ids(m ? m : 1);
-  std::vector<float> dists(m ? m : 1);
-  std::vector<uint8_t> fresh(m ? m : 1);
-  check(rnndg_get_graph(ctx().h, off.data(), ids.data(), dists.data(), fresh.data()));
-  g.adj.assign(n, {});
-  for (uint64_t u = 0; u < n; ++u) {
-    auto& l = g.adj[u];
-    l.reserve(off[u + 1] - off[u]);
-    for (uint64_t j = off[u]; j < off[u + 1]; ++j) l.push_back({ids[j], dists[j], fresh[j] != 0});
-  }
-  g.has_distances = true;
-}
-
-// add_reverse_edges needs no vectors; a 1-d dummy store of the right size
-// satisfies the context when the caller has not bound one
-void bind_any(size_t n) {
-  Ctx& c = ctx();
-  static thread_local std::vector<float> zeros;
-  zeros.assign(n ? n : 1, 0.0f);
-  check(rnndg_set_data(c.h, zeros.data(), n ? n : 1, 1));
-  c.store = nullptr;
-  c.data = zeros.data();
-  c.n = n;
-  c.d = 1;
-}
-
-}  // namespace
+using shim::bind_any;
+using shim::bind_store;
+using shim::check;
+using shim::ctx;
+using shim::download;
+using shim::upload;
 
 std::vector<NeighborEntry> rng_strategy(const VectorStore& store, uint32_t u,
                                         std::vector<NeighborEntry> candidates) {
