@@ -219,6 +219,27 @@ int rnndg_shard_import(rnndg_ctx* ctx, int kind, const uint32_t* dst_dev,
                        rnndg_counts* partial, uint64_t* nstaged);
 int rnndg_shard_out_prune(rnndg_ctx* ctx, uint32_t R);
 
+/* ---- vertex-sharded build in one process (builder.cpp:253-289 over
+ * shards; csrc/multi.cu) ----
+ * Shard i runs on CUDA device devs[i] (repeats allowed: several shards may
+ * share a GPU) and owns a contiguous vertex range; records move between
+ * shards by peer copies (NVLink / NVSwitch between B200s).  The graph and
+ * every pass count equal rnndg_build's. */
+typedef struct rnndg_sharded rnndg_sharded;
+int rnndg_sharded_create(rnndg_sharded** out, const int* devs, int nshards);
+int rnndg_sharded_destroy(rnndg_sharded* h);
+const char* rnndg_sharded_last_error(const rnndg_sharded* h);
+int rnndg_sharded_set_data(rnndg_sharded* h, const float* rows, uint64_t n, uint32_t d);
+/* fills seconds, update_passes, reverse_phases, edits, kernel_launches */
+int rnndg_sharded_build(rnndg_sharded* h, uint32_t S, uint32_t R, uint32_t T1, uint32_t T2,
+                        uint64_t seed, int order, rnndg_build_stats* stats);
+int rnndg_sharded_pass_counts(rnndg_sharded* h, rnndg_counts* out, uint32_t cap,
+                              uint32_t* npasses);
+int rnndg_sharded_graph_size(rnndg_sharded* h, uint64_t* n, uint64_t* edges);
+/* the whole graph, lists in vertex order (CSR; any of ids/dists/fresh may be NULL) */
+int rnndg_sharded_get_graph(rnndg_sharded* h, uint64_t* offsets, uint32_t* ids, float* dists,
+                            uint8_t* fresh);
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,16 @@ def lib() -> C.CDLL:
         "rnndg_shard_import": (C.c_int, [vp, C.c_int, vp, vp, C.c_uint64, C.c_uint32,
                                          C.POINTER(Counts), u64p]),
         "rnndg_shard_out_prune": (C.c_int, [vp, C.c_uint32]),
+        "rnndg_sharded_create": (C.c_int, [C.POINTER(vp), C.POINTER(C.c_int), C.c_int]),
+        "rnndg_sharded_destroy": (C.c_int, [vp]),
+        "rnndg_sharded_last_error": (C.c_char_p, [vp]),
+        "rnndg_sharded_set_data": (C.c_int, [vp, f32p, C.c_uint64, C.c_uint32]),
+        "rnndg_sharded_build": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
+                                          C.c_uint64, C.c_int, C.POINTER(BuildStatsC)]),
+        "rnndg_sharded_pass_counts": (C.c_int, [vp, C.POINTER(Counts), C.c_uint32,
+                                                C.POINTER(C.c_uint32)]),
+        "rnndg_sharded_graph_size": (C.c_int, [vp, u64p, u64p]),
+        "rnndg_sharded_get_graph": (C.c_int, [vp, u64p, u32p, f32p, u8p]),
         "rnndg_nnd_init": (C.c_int, [vp, C.c_uint32, C.c_uint32, C.c_uint32, C.c_uint32,
                                      C.c_uint64]),
         "rnndg_nnd_pass": (C.c_int, [vp, u64p]),
@@ -123,4 +133,7 @@ EXPORTED = (
     "rnndg_shard_import", "rnndg_shard_out_prune", "rnndg_shard_totals",
     "rnndg_nnd_init", "rnndg_nnd_pass", "rnndg_nnd_pools", "rnndg_nnd_finalize",
     "rnndg_nnd_build",
+    "rnndg_sharded_create", "rnndg_sharded_destroy", "rnndg_sharded_last_error",
+    "rnndg_sharded_set_data", "rnndg_sharded_build", "rnndg_sharded_pass_counts",
+    "rnndg_sharded_graph_size", "rnndg_sharded_get_graph",
 )

@@ -264,3 +264,70 @@ def sharded_build(engines, transport, n: int, world: int, S=20, R=96, T1=4, T2=1
                 for e in engines:
                     e.out_prune(R)
     return st
+
+
+# ------------------------------------------------- one process, C ABI only
+
+class MultiDevice:
+    """rnndg_sharded_* (csrc/multi.cu): the same protocol run by the library
+    itself over several device contexts in this process -- records move by
+    peer copies, no torch.  ``devices`` may repeat (shards sharing a GPU)."""
+
+    def __init__(self, devices: Sequence[int]):
+        self._L = _lib.lib()
+        self.h = C.c_void_p()
+        arr = (C.c_int * len(devices))(*devices)
+        rc = self._L.rnndg_sharded_create(C.byref(self.h), arr, len(devices))
+        self._check(rc)
+
+    def _check(self, rc):
+        if rc != _lib.OK:
+            msg = self._L.rnndg_sharded_last_error(self.h).decode() if self.h else "create failed"
+            from .rnnd import ParamError, DataError
+            if rc == _lib.EPARAM:
+                raise ParamError(msg)
+            if rc == _lib.EDATA:
+                raise DataError(msg)
+            raise RuntimeError(msg)
+
+    def close(self):
+        if self.h:
+            self._L.rnndg_sharded_destroy(self.h)
+            self.h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_data(self, data: np.ndarray):
+        self._data = np.ascontiguousarray(data, np.float32)
+        n, d = self._data.shape
+        self._check(self._L.rnndg_sharded_set_data(self.h, self._data.ctypes.data_as(_lib.f32p),
+                                                   n, d))
+
+    def build(self, S=20, R=96, T1=4, T2=15, seed=42, order=0):
+        st = _lib.BuildStatsC()
+        self._check(self._L.rnndg_sharded_build(self.h, S, R, T1, T2, seed, order, C.byref(st)))
+        npass = C.c_uint32()
+        self._check(self._L.rnndg_sharded_pass_counts(self.h, None, 0, C.byref(npass)))
+        pc = (_lib.Counts * max(npass.value, 1))()
+        self._check(self._L.rnndg_sharded_pass_counts(self.h, pc, npass.value, C.byref(npass)))
+        counts = [[c.removed, c.inserted, c.flag_skips, c.pair_checks]
+                  for c in pc[:npass.value]]
+        return st, counts
+
+    def get_graph(self):
+        from .rnnd import CSR
+        n, m = C.c_uint64(), C.c_uint64()
+        self._check(self._L.rnndg_sharded_graph_size(self.h, C.byref(n), C.byref(m)))
+        off = np.empty(n.value + 1, np.uint64)
+        ids = np.empty(max(m.value, 1), np.uint32)
+        dists = np.empty(max(m.value, 1), np.float32)
+        fresh = np.empty(max(m.value, 1), np.uint8)
+        self._check(self._L.rnndg_sharded_get_graph(
+            self.h, off.ctypes.data_as(_lib.u64p), ids.ctypes.data_as(_lib.u32p),
+            dists.ctypes.data_as(_lib.f32p), fresh.ctypes.data_as(_lib.u8p)))
+        mm = m.value
+        return CSR(off, ids[:mm], dists[:mm], fresh[:mm])
