@@ -71,6 +71,7 @@
 // (A warp-specialised single-CTA version, producers / MMA / epilogue warps
 // with mbarrier rings, ran its epilogue on 4 warps only and was latency-bound
 // there: 2.5 s per C3 1M build.)
+#include <cstddef>
 #include <cstdio>
 #include <cstdlib>
 
@@ -92,7 +93,7 @@ constexpr uint32_t kSub = 32;        // k elements per SW64 operand sub-tile
 constexpr int kNR = 3;               // ring stages (raw fp32 chunk -> bf16 operands in place)
 constexpr int kLA = 1;               // chunks in flight ahead of the one being converted
 constexpr uint32_t kOpBytes = 8192;  // 128 rows x 32 bf16 (SWIZZLE_64B)
-constexpr uint32_t kTmemCols = 128;
+constexpr uint32_t kTmemCols = 256;  // HH^T at columns 0..127, HL^T at 128..255
 constexpr uint32_t kAQ = 512;        // band comparisons resolved per round
 
 // RNNDG_TRACE: cycles per phase (thread 0 of every CTA), summed over CTAs
@@ -105,6 +106,10 @@ enum GramProf : int {
   kPfTotal,
   kPfAmbPairs,    // band comparisons evaluated
   kPfTiles,
+  kPfIssue,     // stream, warp 1: next chunk's copies (incl. waiting for a free stage)
+  kPfCpWait,    //   waiting for this chunk's copies
+  kPfConv,      //   conversion .. arrival
+  kPfMmaIssue,  // warp 0: waiting for all warps' chunk, then issuing the MMAs
   kPfNum
 };
 
@@ -156,6 +161,12 @@ struct GramSmem {
   uint32_t cls, nl, first, naq, tmem_base;
   uint64_t st_full[kNR], st_free[kNR], acc_ready;
 };
+
+static_assert(offsetof(GramSmem, craw) == offsetof(GramSmem, ring) + sizeof(GramSmem::ring),
+              "the epilogue scratch spans ring and craw");
+static_assert(sizeof(GramSmem::ring) + sizeof(GramSmem::craw) >=
+                  (128u * 129u + kWarps * 1024u) * sizeof(float),
+              "staged HL^T + pair scratch must fit the idle ring");
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(smem)), "l"(gmem)
@@ -378,9 +389,14 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
     float sch[2] = {0.f, 0.f};  // chain cv_c of the two rows
     float stl[2][3] = {};       // squared tail terms (unit 0 of block nblk)
     for (uint32_t ch = 0; ch < nch; ++ch) {
+      long long c0 = clock64();
       issue(ch + kLA);
+      long long c1 = clock64();
       cp_async_wait<kLA>();
       __syncwarp();  // this warp's copies of chunk ch landed
+      long long c2 = clock64();
+      pf[kPfIssue] += c1 - c0;
+      pf[kPfCpWait] += c2 - c1;
       const uint32_t gi = gch + ch, st = gi % kNR, use = gi / kNR;
       uint8_t* stage = sm.ring[st];
       uint64_t t[2][2][4];  // [row item][block][pair]
@@ -438,9 +454,15 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
       tc::fence_async_smem();
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&sm.st_full[st]);
+      {
+        const long long c3 = clock64();
+        pf[kPfConv] += c3 - c2;
+        c2 = c3;
+      }
       if (wid == 0) {
         if (lane == 0) {
           tc::mbar_wait(&sm.st_full[st], use & 1u);
+          pf[kPfMmaIssue] += clock64() - c2;
           tc::tc_fence_after();
 #pragma unroll
           for (uint32_t bb = 0; bb < 2; ++bb) {
@@ -448,9 +470,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
 #pragma unroll
             for (uint32_t k = 0; k < kSub / 16; ++k) {
               const uint64_t dh = tc::sw64_desc(ha + 32 * k), dl = tc::sw64_desc(la + 32 * k);
-              tc::mma_bf16(tmem, dh, dh, idesc, (ch | bb | k) ? 1u : 0u);
-              tc::mma_bf16(tmem, dh, dl, idesc, 1u);
-              tc::mma_bf16(tmem, dl, dh, idesc, 1u);
+              // G = HH^T + HL^T + (HL^T)^T: the third product is the
+              // transpose of the second, added in the epilogue (2 MMAs, not 3)
+              const uint32_t acc = (ch | bb | k) ? 1u : 0u;
+              tc::mma_bf16(tmem, dh, dh, idesc, acc);
+              tc::mma_bf16(tmem + 128u, dh, dl, idesc, acc);
             }
           }
           tc::mma_commit(&sm.st_free[st]);
@@ -498,17 +522,32 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
     const uint32_t Ue = sl_e < nl ? sm.lU[sl_e] : 0u;
     const bool real = e - s0 < Ue;
     float v[32];
+    // HL^T rows of the tile in shared memory (the ring is idle now), row
+    // stride 129 floats: thread e reads HL[e][j] and HL[j][e] conflict-free
+    float* hls = reinterpret_cast<float*>(sm.ring[0]);
+    const uint32_t blo = ((32u * q) & ~(R - 1u)) >> 5;        // column blocks of
+    const uint32_t bhi = ((32u * q + 31u) | (R - 1u)) >> 5;   // these rows' lists
     if (h == 0) {
-      tc::tmem_ld32(tb + 32u * q, v);  // the diagonal block of these rows
-      float dg = v[0];
+      tc::tmem_ld32(tb + 32u * q, v);  // the diagonal blocks of these rows
+      float hh = v[0];
 #pragma unroll
       for (int j = 1; j < 32; ++j)
-        if (uint32_t(j) == lane) dg = v[j];
-      sm.diag[e] = dg;
+        if (uint32_t(j) == lane) hh = v[j];
+      tc::tmem_ld32(tb + 128u + 32u * q, v);
+      float hl = v[0];
+#pragma unroll
+      for (int j = 1; j < 32; ++j)
+        if (uint32_t(j) == lane) hl = v[j];
+      sm.diag[e] = __fadd_rn(hh, __fadd_rn(hl, hl));  // G_ee = HH + HL + LH
       sm.rank[e] = 0u;
     }
+    for (uint32_t cb = blo + h; cb <= bhi; cb += 2) {
+      tc::tmem_ld32(tb + 128u + 32u * cb, v);
+#pragma unroll
+      for (int jj = 0; jj < 32; ++jj) hls[e * 129u + 32u * cb + uint32_t(jj)] = v[jj];
+    }
     if (tid == 0) sm.naq = 0;
-    __syncthreads();  // keys final (pending filled), diag, rank zeroed
+    __syncthreads();  // keys final (pending filled), diag, HL^T staged, rank zeroed
     const uint64_t ke = sm.key[e];
     if (real) {  // rank by (dist, id) within the list, halves split by parity
       uint32_t r = 0;
@@ -529,19 +568,19 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
     const float dg = sm.diag[e];
     uint32_t oc[4] = {0u, 0u, 0u, 0u}, am[4] = {0u, 0u, 0u, 0u};
     {
-      const uint32_t lo = ((32u * q) & ~(R - 1u)) >> 5;
-      const uint32_t hi = ((32u * q + 31u) | (R - 1u)) >> 5;
-      for (uint32_t cb = lo + h; cb <= hi; cb += 2) {
-        tc::tmem_ld32(tb + 32u * cb, v);
+      for (uint32_t cb = blo + h; cb <= bhi; cb += 2) {
+        tc::tmem_ld32(tb + 32u * cb, v);  // HH^T
         if (!real) continue;
 #pragma unroll
         for (int jj = 0; jj < 32; ++jj) {
           const uint32_t j = 32u * cb + uint32_t(jj);
           if (j - s0 >= Ue || j == e) continue;
           if (!(sm.key[j] < ke)) continue;
+          const float gij =
+              __fadd_rn(__fadd_rn(v[jj], hls[e * 129u + j]), hls[j * 129u + e]);
           const float dj = sm.diag[j];
           const float sn = __fadd_rn(fabsf(dg), fabsf(dj));
-          const float dd = __fsub_rn(__fadd_rn(dg, dj), __fmul_rn(2.f, v[jj]));
+          const float dd = __fsub_rn(__fadd_rn(dg, dj), __fmul_rn(2.f, gij));
           const float eps = __fadd_rn(__fmul_rn(sn, g.eps_rel), 1e-25f);
           const uint32_t pj = sm.pos[j];
           if (__fadd_rn(dd, eps) < thr)
@@ -568,7 +607,8 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
       const bool fe = key_fresh(ke);
       bool more = real;
       uint32_t w4 = 0;
-      float* scratch = reinterpret_cast<float*>(sm.ring[0]) + wid * 1024u;  // 4 KB per warp
+      // 4 KB per warp past the staged HL^T (ring + centre buffers are contiguous)
+      float* scratch = reinterpret_cast<float*>(sm.ring[0]) + 128u * 129u + wid * 1024u;
       for (;;) {
         if (more) {
           more = false;
@@ -723,8 +763,11 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
   }
   if (g.prof && tid == 0) {
     pf[kPfTotal] = clock64() - p0;
-    for (int i = 0; i < kPfNum; ++i) atomicAdd(&g.prof[i], (unsigned long long)pf[i]);
+    for (int i = 0; i < kPfIssue; ++i) atomicAdd(&g.prof[i], (unsigned long long)pf[i]);
+    atomicAdd(&g.prof[kPfMmaIssue], (unsigned long long)pf[kPfMmaIssue]);
   }
+  if (g.prof && tid == 32)
+    for (int i = kPfIssue; i < kPfMmaIssue; ++i) atomicAdd(&g.prof[i], (unsigned long long)pf[i]);
   for (int o = 16; o; o >>= 1) {
     removed += __shfl_xor_sync(0xffffffffu, removed, o);
     checks += __shfl_xor_sync(0xffffffffu, checks, o);
@@ -842,16 +885,15 @@ void gram_trace(rnndg_ctx* c) {
   if (!gram_cap() || !c->gram_prof.p) return;
   unsigned long long h[kPfNum];
   RNNDG_CUDA(cudaMemcpy(h, c->gram_prof.p, sizeof(h), cudaMemcpyDeviceToHost));
-  int per_sm = 0;
-  RNNDG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_scan_gram, kThreads,
-                                                           sizeof(GramSmem) + 1024));
-  const double ctas = double(sm_count(c) * (per_sm > 0 ? per_sm : 1));
+  const double ctas = double(sm_count(c) * kCtasPerSm);
   auto mc = [&](int i) { return double(h[i]) / ctas * 1e-6; };  // Mcycles per CTA
   std::fprintf(stderr,
-               "[rnndg] gram: tiles=%llu per CTA %.2f Mcyc: stream %.2f mma-wait %.2f mask %.2f "
+               "[rnndg] gram: tiles=%llu per CTA %.2f Mcyc: stream %.2f (warp 1: issue %.2f "
+               "copy-wait %.2f convert %.2f; warp 0 mma-gate %.2f) mma-wait %.2f mask %.2f "
                "amb %.2f (%llu pairs) walk %.2f\n",
-               h[kPfTiles], mc(kPfTotal), mc(kPfStream), mc(kPfMmaWait), mc(kPfMask), mc(kPfAmb),
-               h[kPfAmbPairs], mc(kPfWalk));
+               h[kPfTiles], mc(kPfTotal), mc(kPfStream), mc(kPfIssue), mc(kPfCpWait), mc(kPfConv),
+               mc(kPfMmaIssue), mc(kPfMmaWait), mc(kPfMask), mc(kPfAmb), h[kPfAmbPairs],
+               mc(kPfWalk));
 }
 
 }  // namespace rnndg
