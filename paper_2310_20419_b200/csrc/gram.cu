@@ -278,7 +278,7 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
   tc::tc_fence_after();
   const uint32_t tmem = sm.tmem_base;
   const Row row = g.row;
-  constexpr uint32_t idesc = tc::idesc_bf16_f32<128, 128>();
+  constexpr uint32_t idesc256 = tc::idesc_bf16_f32<128, 256>();
   // epilogue mapping: TMEM lane quarter q, column half h; tile row e
   const uint32_t q = wid & 3u, h = wid >> 2, e = 32u * q + lane;
   unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, namb = 0;
@@ -470,11 +470,12 @@ __global__ void __launch_bounds__(kThreads, kCtasPerSm) k_scan_gram(GramArgs g) 
 #pragma unroll
             for (uint32_t k = 0; k < kSub / 16; ++k) {
               const uint64_t dh = tc::sw64_desc(ha + 32 * k), dl = tc::sw64_desc(la + 32 * k);
-              // G = HH^T + HL^T + (HL^T)^T: the third product is the
-              // transpose of the second, added in the epilogue (2 MMAs, not 3)
-              const uint32_t acc = (ch | bb | k) ? 1u : 0u;
-              tc::mma_bf16(tmem, dh, dh, idesc, acc);
-              tc::mma_bf16(tmem + 128u, dh, dl, idesc, acc);
+              // G = HH^T + HL^T + (HL^T)^T: ONE M128 x N256 MMA whose B is
+              // the hi tile followed by the lo tile (contiguous, same
+              // SBO), so TMEM columns 0..127 get HH^T and 128..255 HL^T;
+              // the LH^T term is HL^T transposed, added in the epilogue
+              (void)dl;
+              tc::mma_bf16(tmem, dh, dh, idesc256, (ch | bb | k) ? 1u : 0u);
             }
           }
           tc::mma_commit(&sm.st_free[st]);
