@@ -152,9 +152,10 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
       act = __any_sync(0xffffffffu, j < U && key_fresh(key[b + j]));
     }
     if (lane != 0) continue;
-    if (mat_b && act && U > gcap && key_pending(key[b + U - 1])) {
-      // an active list the Gram walk does not take, ending in pending
-      // entries (they sort last): queued for resolve_pending before the scan
+    if (mat_b && act && U > ucap && key_pending(key[b + U - 1])) {
+      // an active hub list ending in pending entries (they sort last):
+      // queued for resolve_pending before the scan (the Gram walk and the
+      // short-list kernel resolve their own lists' pending entries)
       const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kMatCount]), 1u);
       mat_b[x] = b;
       mat_e[x] = b + U;
@@ -1070,8 +1071,114 @@ __global__ void __launch_bounds__(kBlock)
   }
 }
 
+// after k_resolve_merge: queue entries it finished become empty ranges,
+// the ones it flagged (tail too long) keep theirs for resolve_pending
+__global__ void __launch_bounds__(kBlock)
+    k_flagged_only(uint64_t n, uint64_t* __restrict__ mat_b, uint64_t* __restrict__ mat_e,
+                   const unsigned long long* __restrict__ count) {
+  const uint64_t nq = *count;
+  for (uint64_t x = uint64_t(blockIdx.x) * blockDim.x + threadIdx.x; x < nq;
+       x += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t u = mat_e[n + x];
+    if (u >> 63) {
+      mat_e[n + x] = u & ~(1ull << 63);
+    } else {
+      mat_e[x] = mat_b[x];
+    }
+  }
+}
+
+// Hub lists with pending entries, one CTA per list: the pending tail (it
+// sorts last) is resolved by the CTA's quads, sorted in shared memory and
+// merged with the sorted prefix by ranks -- O(U) instead of a full segmented
+// sort of a list of thousands.  Tails longer than kMergeCap are left for
+// the segmented sort (flagged by setting mat_e[n + x] |= 1 << 63).
+constexpr uint32_t kMergeCap = 2048;
+constexpr int kMergeThreads = 256;
+
+__global__ void __launch_bounds__(kMergeThreads)
+    k_resolve_merge(uint64_t n, uint64_t v0, const uint64_t* __restrict__ mat_b,
+                    uint64_t* __restrict__ mat_e, const unsigned long long* __restrict__ count,
+                    uint64_t* __restrict__ key, uint64_t* __restrict__ scratch, Row row) {
+  __shared__ uint64_t tail[kMergeCap];
+  __shared__ uint32_t s_p0;
+  const uint32_t tid = threadIdx.x, lane = lane_id(), quad = tid >> 2, chain = lane & 3;
+  const uint64_t nq = *count;
+  for (uint64_t x = blockIdx.x; x < nq; x += gridDim.x) {
+    const uint64_t b = mat_b[x], U = mat_e[x] - b, u = mat_e[n + x];
+    uint64_t* L = key + b;
+    if (tid == 0) {  // first pending position: pending keys are the largest
+      uint64_t lo = 0, hi = U;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (key_pending(L[mid])) hi = mid; else lo = mid + 1;
+      }
+      s_p0 = uint32_t(lo);
+    }
+    __syncthreads();
+    const uint32_t p0 = s_p0, p = uint32_t(U) - p0;
+    if (p > kMergeCap) {  // rare: the segmented sort after this kernel
+      if (tid == 0) mat_e[n + x] = u | (1ull << 63);
+      __syncthreads();
+      continue;
+    }
+    for (uint32_t i = tid; i < p; i += kMergeThreads) tail[i] = L[p0 + i];
+    __syncthreads();
+    const float* xu = row.xp + (v0 + u) * uint64_t(row.stride);
+    for (uint32_t b0 = 0; b0 < p; b0 += kMergeThreads / 4) {
+      const uint32_t i = b0 + quad;
+      const uint64_t kv = tail[i < p ? i : 0];
+      const float d = quad_l2<false>(row.xp + uint64_t(key_id(kv)) * row.stride, xu, chain,
+                                     row.nblk, row.ntail);
+      if (i < p && chain == 0) tail[i] = make_key(d, key_id(kv), key_fresh(kv));
+    }
+    uint32_t m = 1;
+    while (m < p) m <<= 1;
+    for (uint32_t i = p + tid; i < m; i += kMergeThreads) tail[i] = kTomb;
+    __syncthreads();
+    for (uint32_t k = 2; k <= m; k <<= 1)
+      for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+        for (uint32_t i = tid; i < m; i += kMergeThreads) {
+          const uint32_t l = i ^ jj;
+          if (l > i) {
+            const uint64_t a = tail[i], c = tail[l];
+            if (((i & k) == 0) ? (a > c) : (a < c)) {
+              tail[i] = c;
+              tail[l] = a;
+            }
+          }
+        }
+        __syncthreads();
+      }
+    // merge by ranks into the scratch slice, then back
+    uint64_t* S = scratch + b;
+    for (uint32_t j = tid; j < p0; j += kMergeThreads) {
+      const uint64_t kj = L[j];
+      uint32_t lo = 0, hi = p;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (tail[mid] < kj) lo = mid + 1; else hi = mid;
+      }
+      S[j + lo] = kj;
+    }
+    for (uint32_t i = tid; i < p; i += kMergeThreads) {
+      const uint64_t kt = tail[i];
+      uint64_t lo = 0, hi = p0;
+      while (lo < hi) {
+        const uint64_t mid = (lo + hi) >> 1;
+        if (L[mid] < kt) lo = mid + 1; else hi = mid;
+      }
+      S[i + lo] = kt;
+    }
+    __syncthreads();
+    for (uint64_t j = tid; j < U; j += kMergeThreads) L[j] = S[j];
+    __syncthreads();
+  }
+}
+
 namespace {
 void resolve_pending(rnndg_ctx* c, const unsigned long long* count);
+void resolve_pending_hubs(rnndg_ctx* c, const unsigned long long* count);
 }  // namespace
 
 // Scan phase of a pass: counters zeroed, active vertices marked, locality
@@ -1095,7 +1202,7 @@ void op_scan_phase(rnndg_ctx* c) {
                  c->pending ? c->mat_e.ensure(2 * n) : nullptr);
   if (c->pending && n) {
     prepare_chain_layout(c);
-    resolve_pending(c, c->counters.p + kMatCount);
+    resolve_pending_hubs(c, c->counters.p + kMatCount);
   }
   locality_order(c);
   RNNDG_CUDA(cudaEventRecord(c->ev[1], c->stream));
@@ -1325,6 +1432,20 @@ void resolve_pending(rnndg_ctx* c, const unsigned long long* count) {
   RNNDG_LAUNCH(c, k_resolve_pending, unsigned(sm_count(c)) * 8u, kBlock, 0, n, c->v0, c->mat_b.p,
                c->mat_e.p, count, c->key.p, Row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail});
   seg_sort_keys(c, c->key.p, c->key.p, c->span, n, c->mat_b.p, c->mat_e.p, count);
+}
+
+// the hub lists queued by k_mark_active (few, long, short pending tails)
+void resolve_pending_hubs(rnndg_ctx* c, const unsigned long long* count) {
+  const uint64_t n = c->nv;
+  const ScanConfig cfg = scan_config(c);
+  c->key_s.ensure(c->span ? c->span : 1);
+  RNNDG_LAUNCH(c, k_resolve_merge, unsigned(sm_count(c)) * 4u, kMergeThreads, 0, n, c->v0,
+               c->mat_b.p, c->mat_e.p, count, c->key.p, c->key_s.p,
+               Row{c->xp.p, cfg.stride, cfg.nblk, cfg.ntail});
+  // tails too long for the merge (flagged): quad resolve + segmented sort
+  RNNDG_LAUNCH(c, k_flagged_only, grid_for(n, kBlock), kBlock, 0, n, c->mat_b.p, c->mat_e.p,
+               count);
+  resolve_pending(c, count);
 }
 }  // namespace
 

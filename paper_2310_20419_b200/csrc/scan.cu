@@ -108,6 +108,7 @@ struct ScanArgs {
   int run_tasks; // task budget of an old-run round per 64 threads
   int run_min;   // shortest run taken as an old-run round (0: D + 1)
   int pend;      // redirect records with pending distances (the Gram walk is on)
+  uint64_t v0;   // first owned vertex (partitioned contexts)
 };
 
 __device__ __forceinline__ void flush_counters(unsigned long long* ctr, unsigned long long removed,
@@ -241,6 +242,47 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
     fr0 = __reduce_add_sync(0xffffffffu, fr0);
     if (lane == 0 && fr0) atomicAdd(&s_fr[0], fr0);
     __syncthreads();
+    if (!kLong && g.pend && U && key_pending(keys_sh[U - 1])) {
+      // redirected entries whose distance is pending (gram.cu) sort last:
+      // exact l2_sq(u, v) by the CTA's quads, then the list re-sorted in
+      // shared memory (bitonic over the next power of two, kTomb padding)
+      uint32_t p0 = U;
+      if (tid == 0) s_run = U;  // scratch here: first pending position
+      __syncthreads();
+      for (uint32_t j = tid; j < U; j += NT)
+        if (key_pending(keys_sh[j])) atomicMin(&s_run, j);
+      __syncthreads();
+      p0 = s_run;
+      const float* xu = row.xp + (g.v0 + u) * uint64_t(row.stride);
+      for (uint32_t b0 = p0; b0 < U; b0 += NT / 4) {
+        const uint32_t j = b0 + (tid >> 2);
+        const uint32_t js = j < U ? j : p0;
+        const uint64_t kv = keys_sh[js];
+        const float d = quad_l2<kNA>(row(kv), xu, chain, row.nblk, row.ntail);
+        __syncthreads();
+        if (j < U && chain == 0) keys_sh[j] = make_key(d, key_id(kv), key_fresh(kv));
+        __syncthreads();
+      }
+      uint32_t m = 2;
+      while (m < U) m <<= 1;
+      for (uint32_t j = U + tid; j < m; j += NT) keys_sh[j] = kTomb;
+      __syncthreads();
+      for (uint32_t k = 2; k <= m; k <<= 1)
+        for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+          for (uint32_t i = tid; i < m; i += NT) {
+            const uint32_t l = i ^ jj;
+            if (l > i) {
+              const uint64_t x = keys_sh[i], y = keys_sh[l];
+              const bool up = (i & k) == 0;
+              if (up ? (x > y) : (x < y)) {
+                keys_sh[i] = y;
+                keys_sh[l] = x;
+              }
+            }
+          }
+          __syncthreads();
+        }
+    }
     uint32_t na = U, nk = 0;
     uint32_t rb = 0;  // round parity: s_fr[rb] = fresh alive now, s_fr[rb ^ 1] = next round's
     while (na) {
@@ -1228,6 +1270,7 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   }();
   a.run_min = run_min;
   a.pend = gram_cap() ? 1 : 0;
+  a.v0 = c->v0;
   // two-warp CTAs for short lists (4-warp CTAs measured slower,
   // profiles/README.md)
   constexpr int short_w = kPushWarps;
