@@ -156,9 +156,11 @@ class Device:
     def _evict(self, keep=None):
         o = self._owner() if self._owner is not None else None
         self._owner = None
-        if o is not None and o is not keep and o._dev is self and o._dev_fresh:
-            o._csr = self.get_graph()
-            o._dev_fresh = False
+        if o is not None and o is not keep and o._dev is self:
+            if o._dev_fresh:
+                o._csr = self.get_graph()
+                o._dev_fresh = False
+            o._dev_synced = False  # the slot no longer holds it
         if o is keep and o is not None:
             self._owner = weakref.ref(o)
 
@@ -265,6 +267,7 @@ class AdjacencyGraph:
         self._csr: Optional[CSR] = CSR.empty(n)
         self._dev: Optional[Device] = None
         self._dev_fresh = False  # device holds the newest state
+        self._dev_synced = False  # device slot equals the host copy (after a download)
         self.has_distances = True
 
     # -- construction / views
@@ -279,6 +282,7 @@ class AdjacencyGraph:
         if self._dev_fresh:
             self._csr = self._dev.get_graph()
             self._dev_fresh = False
+            self._dev_synced = True  # the slot still holds exactly this state
             self._host_dirty = False
         return self._csr
 
@@ -292,7 +296,7 @@ class AdjacencyGraph:
             csr = self._host()
             dev.set_data(store)  # evicts the slot's owner
             dev.set_graph(csr, self.has_distances)
-        elif owner is not self or not self._dev_fresh:
+        elif owner is not self or not (self._dev_fresh or self._dev_synced):
             csr = self._host()
             dev._evict(keep=None)
             dev.set_graph(csr, self.has_distances)
@@ -325,6 +329,7 @@ class AdjacencyGraph:
     def set_lists(self, lists):
         self._csr = CSR.from_lists(lists)
         self._dev_fresh = False
+        self._dev_synced = False
 
 
 # ------------------------------------------------------------- builder
