@@ -53,3 +53,15 @@ def test_search_bitmap_rerun_matches(tab):
                         os.path.join(HERE, "test_gpu_parity.py"), "-k", "search"],
                        env=full, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+
+
+@pytest.mark.slow
+def test_gram_walk_fullsize_equals_reference():
+    """The tensor-core Gram walk (RNNDG_GRAM=128) at the BASELINE sizes:
+    the C3 1M x 960 and C4 1M x 96 builds byte-identical to the reference's
+    (tests/test_gpu_fullsize.py in a process with the walk on)."""
+    full = dict(os.environ, RNNDG_GRAM="128")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        os.path.join(HERE, "test_gpu_fullsize.py"), "-k", "C3 or C4"],
+                       env=full, capture_output=True, text=True, timeout=1200)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
