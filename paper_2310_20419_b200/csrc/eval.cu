@@ -469,6 +469,9 @@ void op_search(rnndg_ctx* c, const float* queries, uint64_t nq, uint32_t L,
     const char* e = std::getenv("RNNDG_SEARCH_TAB");
     return e ? std::atoi(e) : 0;
   }();
+  // at most ~512 MB of tables for the whole grid; queries that need more
+  // take the bitmap re-run
+  while (lg > 12 && (uint64_t(4) << lg) * grid > (uint64_t(512) << 20)) --lg;
   if (force_lg >= 4 && force_lg <= 26) lg = uint32_t(force_lg);
   a.tab_log2 = lg;
   a.gtab = c->seen_bits.ensure((uint64_t(1) << lg) * grid);
