@@ -83,6 +83,8 @@ int rnndg_create(rnndg_ctx** out, int device) {
     RNNDG_CUDA(cudaSetDevice(device));
     RNNDG_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
     RNNDG_CUDA(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    RNNDG_CUDA(cudaStreamCreateWithFlags(&c->side2, cudaStreamNonBlocking));
+    RNNDG_CUDA(cudaEventCreateWithFlags(&c->ev_join2, cudaEventDisableTiming));
     RNNDG_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
     RNNDG_CUDA(cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming));
     for (auto& e : c->ev) RNNDG_CUDA(cudaEventCreate(&e));
@@ -109,6 +111,9 @@ int rnndg_destroy(rnndg_ctx* c) {
   for (auto& e : c->ev_scan)
     if (e) cudaEventDestroy(e);
   if (c->side) cudaStreamSynchronize(c->side);
+  if (c->side2) cudaStreamSynchronize(c->side2);
+  if (c->ev_join2) cudaEventDestroy(c->ev_join2);
+  if (c->side2) cudaStreamDestroy(c->side2);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   if (c->ev_join) cudaEventDestroy(c->ev_join);
   if (c->side) cudaStreamDestroy(c->side);

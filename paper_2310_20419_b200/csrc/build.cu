@@ -1197,7 +1197,8 @@ void op_scan_phase(rnndg_ctx* c) {
   if (n)
     RNNDG_LAUNCH(c, k_mark_active, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
-                 big_hub_threshold(c), long_short_threshold(), gram_cap(), c->gram_q.p,
+                 big_hub_threshold(c), bsp_rounds() ? bsp_max_len() : long_short_threshold(),
+                 gram_cap(), c->gram_q.p,
                  c->pending ? c->mat_b.ensure(n) : nullptr,
                  c->pending ? c->mat_e.ensure(2 * n) : nullptr);
   if (c->pending && n) {

@@ -94,6 +94,8 @@ struct rnndg_ctx {
   int device = 0;
   cudaStream_t stream = nullptr;
   cudaStream_t side = nullptr;  // concurrent long-list scan
+  cudaStream_t side2 = nullptr; // concurrent round-synchronous walk (bsp.cu)
+  cudaEvent_t ev_join2 = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::string err;
   uint64_t launches = 0;
@@ -160,6 +162,12 @@ struct rnndg_ctx {
   rnndg::DevBuf<uint64_t> rec_key, rec_key2, part_bounds;
   rnndg::DevBuf<unsigned long long> rec_cursor, part_counts;
   uint64_t rec_n = 0;
+  // round-synchronous walk (bsp.cu): worklists, per-list state, round counters,
+  // the flat task array with its results, per-warp scratch of the last round
+  rnndg::DevBuf<uint32_t> bsp_wl, bsp_state;
+  rnndg::DevBuf<unsigned int> bsp_ctl;
+  rnndg::DevBuf<uint2> bsp_tasks, bsp_itasks;
+  rnndg::DevBuf<float> bsp_res, bsp_ires;
   // chain-blocked copy of the store for the distance stage (scan.cu)
   rnndg::DevBuf<float> xp;
   const float* xp_src = nullptr;

@@ -108,6 +108,7 @@ struct ScanArgs {
   int run_tasks; // task budget of an old-run round per 64 threads
   int run_min;   // shortest run taken as an old-run round (0: D + 1)
   int pend;      // redirect records with pending distances (the Gram walk is on)
+  int skip_small; // act_small is walked by bsp.cu: only the long short lists here
   uint64_t v0;   // first owned vertex (partitioned contexts)
 };
 
@@ -207,7 +208,8 @@ __global__ void __launch_bounds__(32 * W, 1) k_scan_spec(ScanArgs g) {
   const uint32_t row_bytes = row.stride * 4u;
   // short lists: the long ones (act_list[0 ..)) first, then the rest
   const uint32_t nls = kLong ? 0u : uint32_t(g.ctr_in[kLongShortCount]);
-  const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount]) : nls + uint32_t(*g.nsmall);
+  const uint32_t nq = kLong ? uint32_t(g.ctr_in[kLargeCount])
+                            : nls + (g.skip_small ? 0u : uint32_t(*g.nsmall));
   unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, evals = 0;
 
   for (;;) {
@@ -1391,10 +1393,31 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     launch_gram(c, work);
     if (c->trace) RNNDG_CUDA(cudaEventRecord(c->ev_scan[2], c->stream));
   }
+  // RNNDG_BSP: lists of <= bsp_max_len() entries (act_small) are walked round
+  // by round across lists (bsp.cu) on a third stream; the short-list kernel
+  // keeps the longer ones (act_list[0 .. nls))
+  static const int bsp_stream = [] {
+    const char* e = std::getenv("RNNDG_BSP_STREAM");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (bsp_rounds()) {
+    a.skip_small = 1;
+    if (bsp_stream) {
+      RNNDG_CUDA(cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
+      if (bsp_stream == 2) launch_bsp(c, work, c->side2, spec, l2pf);
+    } else {
+      launch_bsp(c, work, c->stream, spec, l2pf);
+    }
+  }
   RNNDG_LAUNCH(c, kshort, grid, threads_short, smem, a);
+  if (bsp_rounds() && bsp_stream == 1) launch_bsp(c, work, c->side2, spec, l2pf);
   if (c->trace) RNNDG_CUDA(cudaEventRecord(c->ev_scan[1], c->stream));
   RNNDG_CUDA(cudaEventRecord(c->ev_join, c->side));
   RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
+  if (bsp_rounds() && bsp_stream) {
+    RNNDG_CUDA(cudaEventRecord(c->ev_join2, c->side2));
+    RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join2, 0));
+  }
 }
 
 }  // namespace rnndg

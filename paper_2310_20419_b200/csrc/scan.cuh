@@ -4,6 +4,8 @@
 #include <cstddef>
 #include <cstdint>
 
+#include <cuda_runtime.h>
+
 struct rnndg_ctx;
 
 namespace rnndg {
@@ -28,6 +30,11 @@ void launch_scan(rnndg_ctx* c, unsigned int* work);
 uint32_t gram_cap();
 void launch_gram(rnndg_ctx* c, unsigned int* work);
 void gram_trace(rnndg_ctx* c);
+// round-synchronous walk of the short lists (bsp.cu; RNNDG_BSP = rounds per
+// pass, 0 = off): lists of at most bsp_max_len() entries, queued in act_small
+int bsp_rounds();
+uint32_t bsp_max_len();
+void launch_bsp(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int spec, int l2pf);
 // provisional entries per push round (RNNDG_SPEC) and the hub-cluster size
 // (0 = one CTA per hub list); build.cu queues big hubs only when clustered
 int spec_mode();

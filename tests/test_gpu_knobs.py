@@ -27,6 +27,16 @@ KNOBS = [
     {"RNNDG_HUB": "0", "RNNDG_LONG_W": "8"},
     {"RNNDG_HUB": "0", "RNNDG_LONG_W": "16"},
     {"RNNDG_UCAP": "128", "RNNDG_LS": "0"},
+    # round-synchronous walk (bsp.cu): all lists finished inside their warps,
+    # two / many rounds, a shorter cut-off, with deeper / shallower speculation,
+    # without the side stream
+    {"RNNDG_BSP": "1"},
+    {"RNNDG_BSP": "2"},
+    {"RNNDG_BSP": "8"},
+    {"RNNDG_BSP": "64", "RNNDG_BSP_LEN": "40"},
+    {"RNNDG_BSP": "6", "RNNDG_SPEC": "4"},
+    {"RNNDG_BSP": "6", "RNNDG_SPEC": "2", "RNNDG_BSP_STREAM": "0"},
+    {"RNNDG_BSP": "12", "RNNDG_BSP_STREAM": "2"},
 ]
 
 
