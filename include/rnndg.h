@@ -210,6 +210,20 @@ int rnndg_shard_stage(rnndg_ctx* ctx, int kind, uint64_t* nrecords);
  * number of records per destination part (bounds: parts+1 vertex ids) */
 int rnndg_shard_export(rnndg_ctx* ctx, const uint64_t* bounds, uint32_t parts,
                        uint32_t* dst_dev, uint64_t* key_dev, uint64_t* counts);
+/* Direct routing of the staged records (the fused exchange; the
+ * pending push of builder.cpp:102-105 across shards): rnndg_shard_route
+ * counts them per destination part (no sort); once the caller has laid out
+ * every owner's receive buffer from all shards' counts, rnndg_shard_push
+ * stores each record straight into its owner's DEVICE buffers
+ * dst_ptrs[p] / key_ptrs[p] from the kernel, starting at offsets[p] (this
+ * shard's segment; order inside it is unspecified, the import is a set
+ * operation).  The buffers may live on another GPU with peer access enabled:
+ * the stores then travel over NVLink.  Returns after the stores are
+ * complete; at most 64 parts. */
+int rnndg_shard_route(rnndg_ctx* ctx, const uint64_t* bounds, uint32_t parts, uint64_t* counts);
+int rnndg_shard_push(rnndg_ctx* ctx, const uint64_t* bounds, uint32_t parts,
+                     uint32_t* const* dst_ptrs, uint64_t* const* key_ptrs,
+                     const uint64_t* offsets);
 /* apply received records (DEVICE buffers); INEDGE stages deletions and
  * returns their number in *nstaged; PENDING reports `inserted`.  The records
  * are read on the library's stream: the caller completes the transfer that

@@ -86,6 +86,9 @@ def lib() -> C.CDLL:
         "rnndg_shard_stage": (C.c_int, [vp, C.c_int, u64p]),
         "rnndg_shard_totals": (C.c_int, [vp, C.POINTER(C.c_double), u64p, u64p, u64p, C.c_int]),
         "rnndg_shard_export": (C.c_int, [vp, u64p, C.c_uint32, vp, vp, u64p]),
+        "rnndg_shard_route": (C.c_int, [vp, u64p, C.c_uint32, u64p]),
+        "rnndg_shard_push": (C.c_int, [vp, u64p, C.c_uint32, C.POINTER(C.c_void_p),
+                                       C.POINTER(C.c_void_p), u64p]),
         "rnndg_shard_import": (C.c_int, [vp, C.c_int, vp, vp, C.c_uint64, C.c_uint32,
                                          C.POINTER(Counts), u64p]),
         "rnndg_shard_out_prune": (C.c_int, [vp, C.c_uint32]),
@@ -130,6 +133,7 @@ EXPORTED = (
     "rnndg_index_bytes", "rnndg_degree_stats", "rnndg_search", "rnndg_brute_force",
     "rnndg_rng_strategy", "rnndg_l2_pairs",
     "rnndg_set_partition", "rnndg_shard_scan", "rnndg_shard_stage", "rnndg_shard_export",
+    "rnndg_shard_route", "rnndg_shard_push",
     "rnndg_shard_import", "rnndg_shard_out_prune", "rnndg_shard_totals",
     "rnndg_nnd_init", "rnndg_nnd_pass", "rnndg_nnd_pools", "rnndg_nnd_finalize",
     "rnndg_nnd_build",

@@ -563,6 +563,25 @@ int rnndg_shard_export(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uin
   });
 }
 
+int rnndg_shard_route(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint64_t* counts) {
+  return guarded(c, [&] {
+    need_graph(c);
+    if (!bounds || !counts) throw ParamError("shard_route: bounds/counts required");
+    op_shard_route(c, bounds, parts, counts);
+  });
+}
+
+int rnndg_shard_push(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts,
+                     uint32_t* const* dst_ptrs, uint64_t* const* key_ptrs,
+                     const uint64_t* offsets) {
+  return guarded(c, [&] {
+    need_graph(c);
+    if (!bounds || !dst_ptrs || !key_ptrs || !offsets)
+      throw ParamError("shard_push: bounds/buffers/offsets required");
+    op_shard_push(c, bounds, parts, dst_ptrs, key_ptrs, offsets);
+  });
+}
+
 int rnndg_shard_import(rnndg_ctx* c, int kind, const uint32_t* dst_dev, const uint64_t* key_dev,
                        uint64_t nrecords, uint32_t R, rnndg_counts* partial, uint64_t* nstaged) {
   return guarded(c, [&] {

@@ -605,6 +605,73 @@ __global__ void k_part_counts(uint64_t nr, const uint32_t* __restrict__ rdst,
   counts[p] = lb(bounds[p + 1]) - lb(bounds[p]);
 }
 
+// ---- direct routing of staged records (rnndg_shard_route / rnndg_shard_push)
+constexpr uint32_t kMaxParts = 64;
+struct PushArgs {
+  uint32_t* dst[kMaxParts];   // receive buffers of every part's owner (peer-mapped
+  uint64_t* key[kMaxParts];   //   over NVLink when the owner is another device)
+  uint64_t at[kMaxParts];     // where this shard's segment starts in them
+  uint64_t bounds[kMaxParts + 1];
+  uint32_t parts;
+};
+
+__device__ __forceinline__ uint32_t part_of(const uint64_t* bounds, uint32_t parts, uint32_t v) {
+  uint32_t lo = 0, hi = parts;  // bounds[lo] <= v < bounds[hi]
+  while (hi - lo > 1) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (bounds[mid] <= v)
+      lo = mid;
+    else
+      hi = mid;
+  }
+  return lo;
+}
+
+// records per destination part, unsorted records (warp-aggregated by part)
+__global__ void __launch_bounds__(256)
+    k_route_counts(uint64_t nr, const uint32_t* __restrict__ rdst, PushArgs a,
+                   unsigned long long* __restrict__ counts) {
+  __shared__ unsigned long long s_cnt[kMaxParts];
+  if (threadIdx.x < kMaxParts) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  for (uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x; i0 < nr;
+       i0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    const bool has = i < nr;
+    const uint32_t p = has ? part_of(a.bounds, a.parts, rdst[i]) : kMaxParts;
+    const unsigned peers = __match_any_sync(0xffffffffu, p);
+    if (has && lane_id() == uint32_t(__ffs(peers)) - 1u)
+      atomicAdd(&s_cnt[p], (unsigned long long)__popc(peers));
+  }
+  __syncthreads();
+  if (threadIdx.x < a.parts && s_cnt[threadIdx.x]) atomicAdd(&counts[threadIdx.x], s_cnt[threadIdx.x]);
+}
+
+// every staged record stored straight into its owner's receive buffers: the
+// position inside this shard's segment comes from a local cursor per part
+// (one atomic per warp and part), the stores go to peer memory
+__global__ void __launch_bounds__(256)
+    k_route_push(uint64_t nr, const uint32_t* __restrict__ rdst, const uint64_t* __restrict__ rkey,
+                 PushArgs a, unsigned long long* __restrict__ cursor) {
+  for (uint64_t i0 = uint64_t(blockIdx.x) * blockDim.x; i0 < nr;
+       i0 += uint64_t(gridDim.x) * blockDim.x) {
+    const uint64_t i = i0 + threadIdx.x;
+    const bool has = i < nr;
+    const uint32_t d = has ? rdst[i] : 0u;
+    const uint32_t p = has ? part_of(a.bounds, a.parts, d) : kMaxParts;
+    const unsigned peers = __match_any_sync(0xffffffffu, p);
+    const uint32_t leader = uint32_t(__ffs(peers)) - 1u;
+    unsigned long long at = 0;
+    if (has && lane_id() == leader) at = atomicAdd(&cursor[p], (unsigned long long)__popc(peers));
+    at = __shfl_sync(0xffffffffu, at, leader);
+    if (has) {
+      const uint64_t pos = a.at[p] + at + __popc(peers & ((1u << lane_id()) - 1u));
+      a.dst[p][pos] = d;
+      a.key[p][pos] = rkey[i];
+    }
+  }
+}
+
 
 // ------------------------------------------------------------- host glue
 
@@ -1561,6 +1628,58 @@ void op_shard_export(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint3
   RNNDG_CUDA(cudaMemcpyAsync(counts, c->part_counts.p, parts * 8, cudaMemcpyDeviceToHost,
                              c->stream));
   RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+// Direct routing (the fused exchange of SURVEY 8(e)): instead of sorting the
+// staged records by destination and handing them to a transport, count them
+// per owner (op_shard_route), and -- once the caller has laid out every
+// owner's receive buffer from all shards' counts -- store each record
+// straight into its owner's buffer from the kernel (op_shard_push; the
+// buffers are peer-mapped when the owner is another GPU, so the stores travel
+// over NVLink).  No sort, no staging copy, no collective.
+namespace {
+PushArgs push_args(const uint64_t* bounds, uint32_t parts) {
+  if (parts == 0 || parts > kMaxParts) throw ParamError("shard routing: 1 .. 64 parts");
+  PushArgs a{};
+  a.parts = parts;
+  for (uint32_t p = 0; p <= parts; ++p) a.bounds[p] = bounds[p];
+  return a;
+}
+}  // namespace
+
+void op_shard_route(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint64_t* counts) {
+  const uint64_t nr = c->rec_n;
+  PushArgs a = push_args(bounds, parts);
+  c->part_counts.ensure(2 * kMaxParts);
+  zero(c, c->part_counts.p, 2 * kMaxParts);
+  if (nr)
+    RNNDG_LAUNCH(c, k_route_counts, grid_for(nr, 256, unsigned(sm_count(c)) * 8u), 256, 0, nr,
+                 c->rec_dst.p, a, c->part_counts.p);
+  static_assert(sizeof(unsigned long long) == sizeof(uint64_t), "");
+  RNNDG_CUDA(cudaMemcpyAsync(counts, c->part_counts.p, parts * 8, cudaMemcpyDeviceToHost,
+                             c->stream));
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+}
+
+void op_shard_push(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint32_t* const* dst_ptrs,
+                   uint64_t* const* key_ptrs, const uint64_t* offsets) {
+  const uint64_t nr = c->rec_n;
+  if (nr) {
+    PushArgs a = push_args(bounds, parts);
+    for (uint32_t p = 0; p < parts; ++p) {
+      a.dst[p] = dst_ptrs[p];
+      a.key[p] = key_ptrs[p];
+      a.at[p] = offsets[p];
+    }
+    c->part_counts.ensure(2 * kMaxParts);
+    unsigned long long* cursor = c->part_counts.p + kMaxParts;
+    zero(c, cursor, kMaxParts);
+    RNNDG_LAUNCH(c, k_route_push, grid_for(nr, 256, unsigned(sm_count(c)) * 8u), 256, 0, nr,
+                 c->rec_dst.p, c->rec_key.p, a, cursor);
+  }
+  // the owners read the records next, on their own streams
+  RNNDG_CUDA(cudaStreamSynchronize(c->stream));
+  c->rec_n = 0;
 }
 
 // received records -> owned lists.  kind: redirects (append-if-absent,

@@ -236,6 +236,9 @@ uint64_t op_export(rnndg_ctx* c, uint64_t* offsets, uint32_t* ids, float* dists,
 uint64_t op_shard_stage(rnndg_ctx* c, int kind);
 void op_shard_export(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint32_t* dst_dev,
                      uint64_t* key_dev, uint64_t* counts);
+void op_shard_route(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint64_t* counts);
+void op_shard_push(rnndg_ctx* c, const uint64_t* bounds, uint32_t parts, uint32_t* const* dst_ptrs,
+                   uint64_t* const* key_ptrs, const uint64_t* offsets);
 uint64_t op_shard_import(rnndg_ctx* c, int kind, const uint32_t* dst_dev, const uint64_t* key_dev,
                          uint64_t nr, uint32_t R, rnndg_counts* partial);
 void op_shard_out_prune(rnndg_ctx* c, uint32_t R);

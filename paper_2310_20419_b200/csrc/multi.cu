@@ -4,18 +4,29 @@
 // Shard i is an rnndg_ctx on CUDA device devs[i] owning the contiguous
 // vertex range [b_i, b_i+1) (rnndg_set_partition); every shard holds the
 // whole store.  Per update pass each shard scans its own lists and stages its
-// redirects as (dst, key) records; the records for shard r are copied
-// straight from every shard's export buffer into r's receive buffer with
-// cudaMemcpyPeerAsync -- NVLink / NVSwitch peer copies between distinct
-// B200s (peer access enabled at creation), device-local copies when shards
-// share a GPU -- and r applies them (rnndg_shard_import).  A reverse phase
-// exchanges proposals, in-edges and deletions the same way (builder.cpp
-// :222-251).  Every step is set-canonical, so the graph and every pass count
-// equal rnndg_build's (tests/test_gpu_multi.py) -- the protocol of
-// paper_2310_20419_b200/sharded.py, with the collective replaced by peer
-// copies issued from the host thread that drives all shards.
+// redirects as (dst, key) records.  The exchange is fused into the producing
+// side: every shard counts its records per owner
+// (rnndg_shard_route), the host lays out each owner's receive buffer from the
+// P x P counts, and one kernel per shard stores every record straight into
+// its owner's buffer (rnndg_shard_push) -- peer-mapped memory over NVLink /
+// NVSwitch between distinct B200s (peer access enabled at creation), plain
+// device memory when shards share a GPU -- with no sort by destination, no
+// staging copy and no collective; then the owner applies them
+// (rnndg_shard_import).  RNNDG_MULTI_EXCHANGE=copy selects the older path
+// (records sorted by destination, cudaMemcpyPeerAsync per segment).  A
+// reverse phase exchanges proposals, in-edges and deletions the same way
+// (builder.cpp:222-251).  Every step is set-canonical, so the graph and every
+// pass count equal rnndg_build's (tests/test_gpu_multi.py) -- the protocol of
+// paper_2310_20419_b200/sharded.py without the collective.  Each phase runs
+// on one host thread per shard, so the shards' kernels overlap across
+// devices; the phases are separated by joins (the exchange is a data
+// dependency between passes).
 #include <algorithm>
 #include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <exception>
+#include <thread>
 #include <string>
 #include <vector>
 
@@ -81,22 +92,84 @@ T* grow(int dev, T* p, uint64_t& cap, uint64_t want) {
   return q;
 }
 
+// fn(s) for every shard, one host thread per shard (the calls block on their
+// device; the devices then work concurrently).  The first failure is rethrown.
+template <class Fn>
+void par_shards(rnndg_sharded* h, Fn fn) {
+  const size_t P = h->ctx.size();
+  if (P == 1) {
+    fn(size_t(0));
+    return;
+  }
+  std::vector<std::exception_ptr> errs(P);
+  std::vector<std::thread> th;
+  th.reserve(P);
+  for (size_t s = 0; s < P; ++s)
+    th.emplace_back([&, s] {
+      try {
+        fn(s);
+      } catch (...) {
+        errs[s] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+}
+
+bool copy_exchange() {
+  const char* e = std::getenv("RNNDG_MULTI_EXCHANGE");
+  return e && std::strcmp(e, "copy") == 0;
+}
+
+void import_all(rnndg_sharded* h, int kind, uint32_t R, const std::vector<uint64_t>& tot,
+                std::vector<rnndg_counts>* partial) {
+  par_shards(h, [&](size_t r) {
+    rnndg_counts pc{};
+    uint64_t ns = 0;
+    chk(h, r, rnndg_shard_import(h->ctx[r], kind, tot[r] ? h->rdst[r] : nullptr,
+                                 tot[r] ? h->rkey[r] : nullptr, tot[r], R, &pc, &ns));
+    h->nstaged[r] = ns;
+    if (partial) (*partial)[r] = pc;
+  });
+}
+
 // every shard's staged records to their owners; then `kind` applied on each
 // receiving shard.  `partial[r]` gets shard r's import counts.
 void exchange(rnndg_sharded* h, int kind, uint32_t R, std::vector<rnndg_counts>* partial) {
   const size_t P = h->ctx.size();
   std::vector<std::vector<uint64_t>> counts(P, std::vector<uint64_t>(P, 0));
-  for (size_t s = 0; s < P; ++s) {
+  std::vector<uint64_t> tot(P, 0);
+  if (!copy_exchange()) {
+    // fused: count per owner, lay out the receive buffers, store into them
+    par_shards(h, [&](size_t s) {
+      chk(h, s, rnndg_shard_route(h->ctx[s], h->bounds.data(), uint32_t(P), counts[s].data()));
+    });
+    for (size_t r = 0; r < P; ++r) {
+      for (size_t s = 0; s < P; ++s) tot[r] += counts[s][r];
+      h->rdst[r] = grow(h->devs[r], h->rdst[r], h->rcap_d[r], tot[r]);
+      h->rkey[r] = grow(h->devs[r], h->rkey[r], h->rcap_k[r], tot[r]);
+    }
+    par_shards(h, [&](size_t s) {
+      std::vector<uint64_t> at(P, 0);  // shard s's segment in owner r's buffer
+      for (size_t r = 0; r < P; ++r)
+        for (size_t q = 0; q < s; ++q) at[r] += counts[q][r];
+      chk(h, s, rnndg_shard_push(h->ctx[s], h->bounds.data(), uint32_t(P), h->rdst.data(),
+                                 h->rkey.data(), at.data()));
+    });
+    import_all(h, kind, R, tot, partial);
+    return;
+  }
+  par_shards(h, [&](size_t s) {
     h->sdst[s] = grow(h->devs[s], h->sdst[s], h->scap_d[s], h->nstaged[s]);
     h->skey[s] = grow(h->devs[s], h->skey[s], h->scap_k[s], h->nstaged[s]);
     chk(h, s, rnndg_shard_export(h->ctx[s], h->bounds.data(), uint32_t(P), h->sdst[s], h->skey[s],
                                  counts[s].data()));
-  }
+  });
   for (size_t r = 0; r < P; ++r) {
-    uint64_t tot = 0;
-    for (size_t s = 0; s < P; ++s) tot += counts[s][r];
-    h->rdst[r] = grow(h->devs[r], h->rdst[r], h->rcap_d[r], tot);
-    h->rkey[r] = grow(h->devs[r], h->rkey[r], h->rcap_k[r], tot);
+    for (size_t s = 0; s < P; ++s) tot[r] += counts[s][r];
+    h->rdst[r] = grow(h->devs[r], h->rdst[r], h->rcap_d[r], tot[r]);
+    h->rkey[r] = grow(h->devs[r], h->rkey[r], h->rcap_k[r], tot[r]);
     RNNDG_CUDA(cudaSetDevice(h->devs[r]));
     uint64_t at = 0;
     for (size_t s = 0; s < P; ++s) {
@@ -110,20 +183,19 @@ void exchange(rnndg_sharded* h, int kind, uint32_t R, std::vector<rnndg_counts>*
                                      m * sizeof(uint64_t), h->copy[r]));
       at += m;
     }
-    // the shard's library stream reads the records next
-    RNNDG_CUDA(cudaStreamSynchronize(h->copy[r]));
-    rnndg_counts pc{};
-    uint64_t ns = 0;
-    chk(h, r, rnndg_shard_import(h->ctx[r], kind, tot ? h->rdst[r] : nullptr,
-                                 tot ? h->rkey[r] : nullptr, tot, R, &pc, &ns));
-    h->nstaged[r] = ns;
-    if (partial) (*partial)[r] = pc;
   }
+  // the shards' library streams read the records next
+  for (size_t r = 0; r < P; ++r) {
+    RNNDG_CUDA(cudaSetDevice(h->devs[r]));
+    RNNDG_CUDA(cudaStreamSynchronize(h->copy[r]));
+  }
+  import_all(h, kind, R, tot, partial);
 }
 
 void in_prune(rnndg_sharded* h, uint32_t R) {
-  for (size_t s = 0; s < h->ctx.size(); ++s)
+  par_shards(h, [&](size_t s) {
     chk(h, s, rnndg_shard_stage(h->ctx[s], RNNDG_X_INEDGE, &h->nstaged[s]));
+  });
   exchange(h, RNNDG_X_INEDGE, R, nullptr);  // stages the deletions
   exchange(h, RNNDG_X_DELETE, R, nullptr);
 }
@@ -202,10 +274,10 @@ int rnndg_sharded_set_data(rnndg_sharded* h, const float* rows, uint64_t n, uint
     if (n < P) throw ParamError("sharded_set_data: fewer vectors than shards");
     h->bounds.resize(P + 1);
     for (size_t r = 0; r <= P; ++r) h->bounds[r] = (n * r) / P;  // sharded.py ownership_bounds
-    for (size_t s = 0; s < P; ++s) {
+    par_shards(h, [&](size_t s) {
       chk(h, s, rnndg_set_data(h->ctx[s], rows, n, d));
       chk(h, s, rnndg_set_partition(h->ctx[s], h->bounds[s], h->bounds[s + 1]));
-    }
+    });
     h->n = n;
   });
 }
@@ -223,13 +295,15 @@ int rnndg_sharded_build(rnndg_sharded* h, uint32_t S, uint32_t R, uint32_t T1, u
     const auto t0 = std::chrono::steady_clock::now();
     rnndg_build_stats st{};
     h->pass_counts.clear();
-    for (size_t s = 0; s < P; ++s) chk(h, s, rnndg_random_init(h->ctx[s], S, seed));
+    par_shards(h, [&](size_t s) { chk(h, s, rnndg_random_init(h->ctx[s], S, seed)); });
     for (uint32_t t1 = 1; t1 <= T1; ++t1) {
       for (uint32_t t2 = 0; t2 < T2; ++t2) {
         rnndg_counts pc{};
-        for (size_t s = 0; s < P; ++s) {
-          rnndg_counts c{};
-          chk(h, s, rnndg_shard_scan(h->ctx[s], &c, &h->nstaged[s]));
+        std::vector<rnndg_counts> sc(P);
+        par_shards(h, [&](size_t s) {
+          chk(h, s, rnndg_shard_scan(h->ctx[s], &sc[s], &h->nstaged[s]));
+        });
+        for (const auto& c : sc) {
           pc.removed += c.removed;
           pc.flag_skips += c.flag_skips;
           pc.pair_checks += c.pair_checks;
@@ -245,15 +319,16 @@ int rnndg_sharded_build(rnndg_sharded* h, uint32_t S, uint32_t R, uint32_t T1, u
         ++st.update_passes;
       }
       if (t1 != T1) {
-        for (size_t s = 0; s < P; ++s)
+        par_shards(h, [&](size_t s) {
           chk(h, s, rnndg_shard_stage(h->ctx[s], RNNDG_X_PROPOSAL, &h->nstaged[s]));
+        });
         exchange(h, RNNDG_X_PROPOSAL, 0, nullptr);
         if (order == RNNDG_OUT_THEN_IN) {
-          for (size_t s = 0; s < P; ++s) chk(h, s, rnndg_shard_out_prune(h->ctx[s], R));
+          par_shards(h, [&](size_t s) { chk(h, s, rnndg_shard_out_prune(h->ctx[s], R)); });
           in_prune(h, R);
         } else {
           in_prune(h, R);
-          for (size_t s = 0; s < P; ++s) chk(h, s, rnndg_shard_out_prune(h->ctx[s], R));
+          par_shards(h, [&](size_t s) { chk(h, s, rnndg_shard_out_prune(h->ctx[s], R)); });
         }
         ++st.reverse_phases;
       }

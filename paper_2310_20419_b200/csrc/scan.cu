@@ -1356,8 +1356,8 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     if (carve >= -1)
       RNNDG_CUDA(cudaFuncSetAttribute(khub, cudaFuncAttributePreferredSharedMemoryCarveout, carve));
     // co-resident clusters, per kernel variant (queried once each)
-    static const void* cached_fn[8] = {};
-    static int cached_clusters[8] = {};
+    static thread_local const void* cached_fn[8] = {};
+    static thread_local int cached_clusters[8] = {};
     int max_clusters = 0;
     int slot = 0;
     for (; slot < 8 && cached_fn[slot]; ++slot)
