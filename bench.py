@@ -526,6 +526,24 @@ def main():
     alg_bytes = 4.0 * cfg.d * st0.touched + 24.0 * st0.active_entries
     achieved = alg_bytes / st0.scan_seconds / 1e9
     peak, peak_src = hbm_peak()
+    # second ceiling of the same stage: the exact no-FMA arithmetic is three
+    # FP32 instructions per element and pair (sub, mul, add), which this B200
+    # issues at 64 lanes per clock and SM (tools/ubench/fp32_pipe.cu, measured;
+    # a flat register-tiled evaluation of dense pair blocks reaches 77% of it,
+    # tools/ubench/flat_pairs.cu).  Counted pairs only (speculative ones are not
+    # algorithmic work).
+    sm_hz = 1965e6
+    try:
+        sm_hz = float(torch.cuda.get_device_properties(local).clock_rate) * 1e3
+    except Exception:
+        pass
+    sms = torch.cuda.get_device_properties(local).multi_processor_count
+    fp32_ops = 3.0 * cfg.d * st0.edits.pair_checks
+    fp32_peak = 64.0 * sms * sm_hz
+    fp32_bound = {"ops_per_build": fp32_ops, "peak_ops_per_s": fp32_peak,
+                  "floor_seconds": fp32_ops / fp32_peak,
+                  "frac": fp32_ops / fp32_peak / st0.scan_seconds,
+                  "peak_source": "64 non-FMA FP32 lanes/clk/SM measured by tools/ubench/fp32_pipe.cu"}
     # DRAM traffic of one distance-stage launch, from the committed ncu
     # --set full capture of this workload (per launch; algorithmic bytes of
     # the same pass alongside)
@@ -608,7 +626,7 @@ def main():
                      "kernel": "k_scan (distance stage)",
                      "algorithmic_bytes_per_build": alg_bytes,
                      "touched": st0.touched, "active_entries": st0.active_entries,
-                     "peak_source": peak_src},
+                     "peak_source": peak_src, "fp32_issue_bound": fp32_bound},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

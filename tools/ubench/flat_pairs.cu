@@ -48,8 +48,15 @@ __device__ __forceinline__ void ld256(const float* p, float (&r)[8]) {
 __device__ __forceinline__ void chain_step(const float (&va)[8], const float (&vb)[8], float& s) {
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
+#ifdef FFMA_IMM
+    float t, m;
+    asm("fma.rn.f32 %0, %1, 0f3F800000, %2;" : "=f"(t) : "f"(va[i]), "f"(-vb[i]));
+    asm("fma.rn.f32 %0, %1, %1, 0f80000000;" : "=f"(m) : "f"(t));
+    asm("fma.rn.f32 %0, %1, 0f3F800000, %2;" : "=f"(s) : "f"(m), "f"(s));
+#else
     const float t = __fsub_rn(va[i], vb[i]);
     s = __fadd_rn(s, __fmul_rn(t, t));
+#endif
   }
 }
 
