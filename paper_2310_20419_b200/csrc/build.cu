@@ -911,7 +911,7 @@ void ensure_scratch(rnndg_ctx* c) {
   c->bcur.ensure(n);
   c->boff.ensure(n + 1);
   c->counters.ensure(kNumCounters);
-  c->work.ensure(8);
+  c->work.ensure(16);
   c->label.ensure(2 * n);
   c->okey.ensure(2 * n);
   c->act_small.ensure(n);
@@ -1255,7 +1255,7 @@ void op_scan_phase(rnndg_ctx* c) {
   ensure_scratch(c);
   unsigned long long* ctr = c->counters.p;
   zero(c, ctr, kNumCounters);
-  zero(c, c->work.p, 8);
+  zero(c, c->work.p, 16);
   zero(c, c->pend_src.p, c->span, 0xFF);
   zero(c, c->touch.p, c->span);
   zero(c, c->bcnt.p, n + 1);
@@ -1265,7 +1265,7 @@ void op_scan_phase(rnndg_ctx* c) {
     RNNDG_LAUNCH(c, k_mark_active, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
                  big_hub_threshold(c), bsp_rounds() ? bsp_max_len() : long_short_threshold(),
-                 gram_cap(), c->gram_q.p,
+                 gram_cap() ? gram_cap() : rowwalk_cap(c), c->gram_q.p,
                  c->pending ? c->mat_b.ensure(n) : nullptr,
                  c->pending ? c->mat_e.ensure(2 * n) : nullptr);
   if (c->pending && n) {
@@ -1585,15 +1585,9 @@ uint64_t op_shard_scan(rnndg_ctx* c, rnndg_counts* partial) {
 // stage reverse proposals (kind 1) or in-edges (kind 2) of the owned lists
 uint64_t op_shard_stage(rnndg_ctx* c, int kind) {
   materialize_pending(c);
-  uint64_t m = 0;
-  {
-    std::vector<uint32_t> cnt(c->nv);
-    if (c->nv)
-      RNNDG_CUDA(cudaMemcpyAsync(cnt.data(), c->cnt.p, c->nv * 4, cudaMemcpyDeviceToHost, c->stream));
-    RNNDG_CUDA(cudaStreamSynchronize(c->stream));
-    for (uint32_t v : cnt) m += v;
-  }
-  ensure_records(c, m);
+  // one record per entry: the span (list capacities) bounds their number, so
+  // no count has to come back to the host to size the buffers
+  ensure_records(c, c->span);
   if (c->nv)
     RNNDG_LAUNCH(c, k_edge_records, warp_grid(c, c->nv), kBlock, 0, c->nv, c->v0, c->off.p,
                  c->cnt.p, c->key.p, c->rec_cursor.p, c->rec_dst.p, c->rec_key.p,

@@ -1,0 +1,470 @@
+// rowwalk.cu -- the push walk (scan_vertex, builder.cpp:41-69; see scan.cu)
+// for SHORT ROWS (d <= ~144: SIFT-like d = 128, Deep-like d = 96), one warp
+// per list with the list's rows resident in shared memory.
+//
+// At d = 960 a pair costs 7.7 KB of row traffic and the walk is bound by the
+// evaluation itself; at d = 96 a pair is 768 B and 288 flops, and the
+// CTA-per-list kernels spend 55-75 SM-cycles per pair on round control and
+// on the memory latency of every round's row loads, ten times the
+// arithmetic.  Here a warp copies all rows of its list into shared memory
+// once (cp.async, one memory round trip per list instead of one per round;
+// a 64-entry list is 25 KB at d = 96) and then runs every round out of
+// shared memory:
+//
+// * alive / touched sets are 32-bit masks (a lane owns positions lane + 32k),
+//   the rounds are k_scan_spec's (an old-run window kept at once, or D
+//   provisional entries whose fates are resolved in list order);
+// * a round's pairs are enumerated kept-entry major into a small task list in
+//   shared memory and evaluated 32 at a time, a lane per pair (every lane
+//   busy: a first version with a lane per candidate, evaluating lazily,
+//   left most lanes idle and was FP32-pipe bound on warp-level executions);
+//   no block barriers anywhere;
+// * rows are stored by list position with a stride of d + 4 floats ((d + 4) / 4
+//   odd), so within a step the lanes' 128-bit reads of consecutive
+//   candidates' rows are bank-conflict free and the kept entry's row is a
+//   broadcast; the exact distance is the reference's four-chain sum read
+//   straight from the row-major store (l2_step4).
+//
+// Lists are queued by size class (<= 16 / 32 / 64 / 128 entries, the queues
+// the Gram walk uses) and each class is a launch with its own shared-memory
+// budget per warp.  Results are the reference's bit for bit: the schedule of
+// rounds never changes pair_checks, flag_skips, removed or a redirect
+// (scan.cu header).
+#include <cstdio>
+#include <cstdlib>
+#include <type_traits>
+
+#include "common.cuh"
+#include "ctx.hpp"
+#include "scan.cuh"
+
+namespace rnndg {
+
+namespace {
+
+constexpr int kMaxD = 4;          // provisional entries per speculative round, at most
+constexpr uint32_t kWin = 16;     // old-run window
+constexpr uint32_t kSmemBudget = 200 * 1024;  // per SM, for the resident rows
+
+struct RowWalkArgs {
+  const uint32_t* queue;      // this class's lists
+  const unsigned long long* count;
+  unsigned int* cursor;
+  const float* x;             // row-major store, 16-byte aligned rows
+  uint32_t d;                 // multiple of 4
+  uint32_t rs;                // row stride in shared memory (floats): d + 4
+  uint32_t max_rows;          // rows per warp region
+  uint32_t warp_bytes;        // shared memory per warp
+  const uint64_t* off;
+  const uint32_t* cnt;
+  uint64_t* keys;
+  uint32_t* post_cnt;
+  uint32_t* pend_src;
+  uint64_t* pend_key;
+  unsigned long long* bcnt;
+  unsigned long long* ctr;
+  int D;
+};
+
+__device__ __forceinline__ uint32_t lt_mask(uint32_t lane) { return (1u << lane) - 1u; }
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(
+                   uint32_t(__cvta_generic_to_shared(smem))),
+               "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.wait_all;" ::: "memory");
+}
+
+// exact l2_sq of two shared-memory rows (metric.hpp:15-24 order; d % 4 == 0)
+__device__ __forceinline__ float dist_rows(const float* a, const float* b, uint32_t q4) {
+  const float4* a4 = reinterpret_cast<const float4*>(a);
+  const float4* b4 = reinterpret_cast<const float4*>(b);
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll 4
+  for (uint32_t c = 0; c < q4; ++c) l2_step4(a4[c], b4[c], s0, s1, s2, s3);
+  return l2_finish(s0, s1, s2, s3);
+}
+
+template <int NP>
+__global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
+  unsigned char* wbase = smem_raw + size_t(wid) * g.warp_bytes;
+  float* rows = reinterpret_cast<float*>(wbase);
+  unsigned char* tail = wbase + size_t(g.max_rows) * g.rs * 4;
+  uint64_t* wk = reinterpret_cast<uint64_t*>(tail);            // window / provisional keys
+  uint32_t* wp = reinterpret_cast<uint32_t*>(tail + 8 * kWin);  // their positions
+  float* fd = reinterpret_cast<float*>(tail + 12 * kWin);       // d(w_j, w_i), [j * kMaxD + i]
+  const uint32_t tcap = kMaxD * g.max_rows;                     // tasks of a round, at most
+  float* res = reinterpret_cast<float*>(tail + 12 * kWin + 4 * kMaxD * kMaxD);  // their distances
+  uint8_t* tpos = reinterpret_cast<uint8_t*>(res + tcap);       // their candidates' positions
+  const uint32_t q4 = g.d >> 2, rs = g.rs;
+  const uint32_t count = uint32_t(*g.count);
+  unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, evals = 0;
+
+  for (;;) {
+    uint32_t it = 0;
+    if (lane == 0) it = atomicAdd(g.cursor, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= count) break;
+    const uint32_t u = g.queue[it];
+    const uint64_t base = g.off[u];
+    const uint32_t U = g.cnt[u];
+    uint64_t* L = g.keys + base;
+    uint64_t kk[NP];
+    uint32_t M[NP], T[NP], F[NP];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const uint32_t p = 32u * k + lane;
+      kk[k] = p < U ? L[p] : 0ull;
+      M[k] = __ballot_sync(0xffffffffu, p < U);
+      F[k] = __ballot_sync(0xffffffffu, p < U && key_fresh(kk[k]));
+      T[k] = 0;
+    }
+    // the list's rows -> shared memory, row r at rows + r * rs
+    __syncwarp();  // the previous list's reads are done
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const uint32_t r1 = U < 32u * (k + 1) ? U : 32u * (k + 1);
+      for (uint32_t r = 32u * k; r < r1; ++r) {
+        const uint32_t id = __shfl_sync(0xffffffffu, key_id(kk[k]), r & 31u);
+        const float* src = g.x + uint64_t(id) * g.d;
+        for (uint32_t c = lane; c < q4; c += 32) cp_async16(rows + r * rs + 4 * c, src + 4 * c);
+      }
+    }
+    cp_async_wait_all();
+    __syncwarp();
+    uint32_t nk = 0;
+
+    for (;;) {
+      // ------------------------------------------------------------ plan
+      uint32_t arank[NP];
+      uint32_t na = 0, nf = 0;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) {
+        arank[k] = na + __popc(M[k] & lt_mask(lane));
+        na += __popc(M[k]);
+        nf += __popc(M[k] & F[k]);
+      }
+      if (na == 0) break;
+      // alive entries ahead of the first fresh one
+      uint32_t run = na;
+      {
+        uint32_t before = 0;
+        bool found = false;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const uint32_t mf = M[k] & F[k];
+          if (!found && mf) {
+            const uint32_t b = uint32_t(__ffs(mf)) - 1u;
+            run = before + __popc(M[k] & lt_mask(b));
+            found = true;
+          }
+          before += __popc(M[k]);
+        }
+      }
+      // a round's pairs are enumerated kept-entry major -- task base[i] + r is
+      // the r-th candidate that needs w_i -- and evaluated 32 at a time, a lane
+      // per pair: within one step the lanes share w_i's row (a broadcast) and
+      // read consecutive candidates' rows (distinct banks)
+      uint32_t frank[NP];
+      {
+        uint32_t f = 0;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          frank[k] = f + __popc(M[k] & F[k] & lt_mask(lane));
+          f += __popc(M[k] & F[k]);
+        }
+      }
+      uint32_t wr = run < kWin ? run : kWin;
+      {
+        const uint32_t cap = tcap / (nf ? nf : 1u);  // window x fresh candidates must fit
+        if (wr > cap) wr = cap;
+      }
+      const bool run_round = wr >= 2;
+      const uint32_t De = run_round ? wr : (na < uint32_t(g.D) ? na : uint32_t(g.D));
+      __syncwarp();
+#pragma unroll
+      for (int k = 0; k < NP; ++k)
+        if ((M[k] >> lane & 1u) && arank[k] < De) {
+          wk[arank[k]] = kk[k];
+          wp[arank[k]] = 32u * k + lane;
+        }
+      uint32_t gone_m[NP], touch_m[NP];
+      if (run_round) {
+        // Old-run round: the window is kept whole (old / old pairs are
+        // skipped, builder.cpp:53-56); every fresh candidate is tested against
+        // it and walks the results in order up to its first occluder.
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+          if (M[k] & F[k] & (1u << lane)) tpos[frank[k]] = uint8_t(32u * k + lane);
+        __syncwarp();
+        const uint32_t ntask = nf * wr;
+        evals += lane == 0 ? ntask : 0u;
+        for (uint32_t t = lane; t < ntask; t += 32) {
+          const uint32_t i = t / nf, r = t - i * nf;
+          res[t] = dist_rows(rows + uint32_t(tpos[r]) * rs, rows + wp[i] * rs, q4);
+        }
+        __syncwarp();
+        uint32_t reach = 0;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          bool gone = false;
+          const bool al = M[k] >> lane & 1u;
+          const bool mine = al && (F[k] >> lane & 1u);
+          if (mine) {
+            const uint64_t vk = kk[k];
+            const uint32_t q = 32u * k + lane;
+            for (uint32_t i = 0; i < wr; ++i) {
+              const float d = res[i * nf + frank[k]];
+              ++checks;
+              reach = reach > i + 1 ? reach : i + 1;
+              if (key_dist(vk) >= d) {
+                gone = true;
+                ++removed;
+                const uint32_t w_id = key_id(wk[i]);
+                g.pend_src[base + q] = w_id;
+                g.pend_key[base + q] = make_key(d, key_id(vk), 1u);
+                if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
+                break;
+              }
+            }
+          } else if (al && arank[k] >= wr) {
+            skips += wr;  // an old candidate behind the window
+          }
+          gone_m[k] = __ballot_sync(0xffffffffu, gone);
+          touch_m[k] = __ballot_sync(0xffffffffu, mine);
+        }
+        reach = __reduce_max_sync(0xffffffffu, reach);
+        if (lane == 0) skips += uint64_t(wr) * (wr - 1) / 2;  // the window among itself
+        __syncwarp();
+        if (lane < wr) L[nk + lane] = wk[lane];  // old already
+        nk += wr;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const bool al = M[k] >> lane & 1u;
+          const uint32_t inwin = __ballot_sync(0xffffffffu, al && arank[k] < wr);
+          const uint32_t tw = __ballot_sync(0xffffffffu, al && arank[k] < reach);
+          T[k] |= touch_m[k] | tw;
+          M[k] &= ~(inwin | gone_m[k]);
+        }
+      } else {
+        // Speculative round: candidate ai >= 1 needs w_i for i < min(ai, De)
+        // where a flag is fresh; the provisional entries w_2 .. w_De are
+        // candidates too (their pairs decide the fates).
+        __syncwarp();
+        uint32_t nm[NP], lim[NP], idx[NP][kMaxD];
+        uint32_t bases[kMaxD + 1];
+        bases[0] = 0;
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const bool al = M[k] >> lane & 1u;
+          const uint32_t ai = arank[k];
+          const bool vf = key_fresh(kk[k]);
+          lim[k] = al ? (ai < De ? ai : De) : 0u;
+          uint32_t m = 0;
+#pragma unroll
+          for (int i = 0; i < kMaxD; ++i)
+            if (uint32_t(i) < lim[k] && (key_fresh(wk[i]) || vf)) m |= 1u << i;
+          nm[k] = m;
+        }
+#pragma unroll
+        for (int i = 0; i < kMaxD; ++i) {
+          uint32_t c = 0;
+#pragma unroll
+          for (int k = 0; k < NP; ++k) {
+            const uint32_t bm = __ballot_sync(0xffffffffu, nm[k] >> i & 1u);
+            idx[k][i] = bases[i] + c + __popc(bm & lt_mask(lane));
+            c += __popc(bm);
+          }
+          bases[i + 1] = bases[i] + c;
+        }
+        const uint32_t ntask = bases[kMaxD];
+        evals += lane == 0 ? ntask : 0u;
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+#pragma unroll
+          for (int i = 0; i < kMaxD; ++i)
+            if (nm[k] >> i & 1u) tpos[idx[k][i]] = uint8_t(32u * k + lane);
+        __syncwarp();
+        for (uint32_t t = lane; t < ntask; t += 32) {
+          uint32_t i = 0;
+#pragma unroll
+          for (int j = 1; j < kMaxD; ++j) i += t >= bases[j] ? 1u : 0u;
+          res[t] = dist_rows(rows + uint32_t(tpos[t]) * rs, rows + wp[i] * rs, q4);
+        }
+        __syncwarp();
+        // the provisional entries publish their pairs; fates in list order,
+        // the same on every lane
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          const uint32_t j = arank[k];
+          if ((M[k] >> lane & 1u) && j >= 1 && j < De)
+#pragma unroll
+            for (int i = 0; i < kMaxD; ++i)
+              if (nm[k] >> i & 1u) fd[j * kMaxD + i] = res[idx[k][i]];
+        }
+        __syncwarp();
+        uint32_t kept = 1u;
+        for (uint32_t j = 1; j < De; ++j) {
+          const float dj = key_dist(wk[j]);
+          bool occl = false;
+          for (uint32_t i = 0; i < j && !occl; ++i) {
+            if (!(key_fresh(wk[i]) || key_fresh(wk[j]))) continue;
+            if ((kept >> i & 1u) && dj >= fd[j * kMaxD + i]) occl = true;
+          }
+          if (!occl) kept |= 1u << j;
+        }
+        uint32_t wtouch = 0;  // provisional entries with a counted check
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          bool gone = false, tch = false;
+          const uint64_t vk = kk[k];
+          const uint32_t q = 32u * k + lane;
+#pragma unroll
+          for (int i = 0; i < kMaxD; ++i) {
+            if (uint32_t(i) >= lim[k] || gone) continue;
+            if (!(kept >> i & 1u)) continue;  // not in the reference's kept list
+            if (!(nm[k] >> i & 1u)) {
+              ++skips;
+              continue;
+            }
+            const float d = res[idx[k][i]];
+            ++checks;
+            tch = true;
+            wtouch |= 1u << i;
+            if (key_dist(vk) >= d) {
+              gone = true;
+              ++removed;
+              const uint32_t w_id = key_id(wk[i]);
+              g.pend_src[base + q] = w_id;
+              g.pend_key[base + q] = make_key(d, key_id(vk), 1u);
+              if (g.bcnt) atomicAdd(&g.bcnt[w_id], 1ull);
+            }
+          }
+          gone_m[k] = __ballot_sync(0xffffffffu, gone);
+          touch_m[k] = __ballot_sync(0xffffffffu, tch);
+        }
+        wtouch = __reduce_or_sync(0xffffffffu, wtouch);
+        __syncwarp();
+        // kept entries, flagged old (builder.cpp:68), in list order
+        {
+          uint32_t n2 = nk;
+#pragma unroll
+          for (int i = 0; i < kMaxD; ++i)
+            if (uint32_t(i) < De && (kept >> i & 1u)) {
+              if (lane == 0) L[n2] = wk[i] & ~1ull;
+              ++n2;
+            }
+          nk = n2;
+        }
+#pragma unroll
+        for (int k = 0; k < NP; ++k) {
+          uint32_t km = 0, tm = 0;
+#pragma unroll
+          for (int i = 0; i < kMaxD; ++i)
+            if (uint32_t(i) < De && (wp[i] >> 5) == uint32_t(k)) {
+              if (kept >> i & 1u) km |= 1u << (wp[i] & 31u);
+              if (wtouch >> i & 1u) tm |= 1u << (wp[i] & 31u);
+            }
+          T[k] |= touch_m[k] | tm;
+          M[k] &= ~(km | gone_m[k]);
+        }
+      }
+    }
+    if (lane == 0) {
+      g.post_cnt[u] = nk;
+      uint32_t tc = 0;
+#pragma unroll
+      for (int k = 0; k < NP; ++k) tc += __popc(T[k]);
+      touched += tc;
+    }
+  }
+  for (int o = 16; o; o >>= 1) {
+    touched += __shfl_xor_sync(0xffffffffu, touched, o);
+    removed += __shfl_xor_sync(0xffffffffu, removed, o);
+    checks += __shfl_xor_sync(0xffffffffu, checks, o);
+    skips += __shfl_xor_sync(0xffffffffu, skips, o);
+    evals += __shfl_xor_sync(0xffffffffu, evals, o);
+  }
+  if (lane == 0) {
+    if (touched) atomicAdd(&g.ctr[kTouched], touched);
+    if (removed) atomicAdd(&g.ctr[kRemoved], removed);
+    if (checks) atomicAdd(&g.ctr[kPairChecks], checks);
+    if (skips) atomicAdd(&g.ctr[kFlagSkips], skips);
+    if (evals) atomicAdd(&g.ctr[kEvalPairs], evals);
+  }
+}
+
+}  // namespace
+
+// Lists of at most this many entries take the shared-memory walk (0 = off):
+// rows of at most 576 bytes with d % 4 == 0 and a 16-byte aligned store,
+// Gram walk off.  RNNDG_ROWWALK = 0 | 16 | 32 | 64 | 128 overrides the cap.
+uint32_t rowwalk_cap(rnndg_ctx* c) {
+  static const int forced = [] {
+    const char* e = std::getenv("RNNDG_ROWWALK");
+    return e ? std::atoi(e) : -1;
+  }();
+  if (forced == 0 || gram_cap() || bsp_rounds()) return 0;
+  if (c->d == 0 || c->d % 4 != 0 || c->d > 144) return 0;
+  if (reinterpret_cast<uintptr_t>(c->x) % 16 != 0) return 0;
+  // measured (C4 1M d = 96: 64 -> 0.537 s, 32 -> 0.561 s, 128 -> 0.573 s, off
+  // 0.765 s; C2 1M d = 128: 32 -> 0.492 s, 64 -> 0.534 s, 128 -> 0.686 s, off
+  // 0.605 s): classes whose rows leave fewer than ~7 warps per SM lose
+  uint32_t cap = c->d <= 100 ? 64 : 32;
+  if (forced > 0) cap = forced <= 16 ? 16 : (forced <= 32 ? 32 : (forced <= 64 ? 64 : 128));
+  return cap;
+}
+
+void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int spec) {
+  const uint32_t cap = rowwalk_cap(c);
+  if (!cap) return;
+  const uint64_t n = c->nv;
+  RowWalkArgs a{};
+  a.x = c->x;
+  a.d = c->d;
+  a.rs = c->d + 4;  // (rs / 4) odd for d % 32 == 0; any d % 4 == 0 keeps 16-byte alignment
+  if ((a.rs / 4) % 2 == 0) a.rs += 4;
+  a.off = c->off.p;
+  a.cnt = c->cnt.p;
+  a.keys = c->key.p;
+  a.post_cnt = c->post_cnt.p;
+  a.pend_src = c->pend_src.p;
+  a.pend_key = c->pend_key.p;
+  a.bcnt = c->partitioned ? nullptr : c->bcnt.p;
+  a.ctr = c->counters.p;
+  a.D = spec < kMaxD ? spec : kMaxD;
+  const uint32_t class_rows[4] = {16, 32, 64, 128};
+  for (int gc = 3; gc >= 0; --gc) {  // the longest walks first
+    if (class_rows[gc] > cap) continue;
+    a.queue = c->gram_q.p + uint64_t(gc) * n;
+    a.count = c->counters.p + kGram0 + gc;
+    a.cursor = work + 8 + gc;
+    a.max_rows = class_rows[gc];
+    a.warp_bytes = a.max_rows * a.rs * 4 + 12 * kWin + 4 * kMaxD * kMaxD +
+                   5 * kMaxD * a.max_rows;  // + task results and positions
+    a.warp_bytes = (a.warp_bytes + 15u) & ~15u;
+    uint32_t warps = kSmemBudget / a.warp_bytes;  // per SM
+    if (warps < 1) continue;
+    if (warps > 32) warps = 32;
+    // CTAs of 4 .. 8 warps, whichever packs the most warps into the budget
+    uint32_t wpc = warps < 8 ? warps : 8, ctas = warps / wpc;
+    for (uint32_t w = 4; w <= 8 && w <= warps; ++w)
+      if ((warps / w) * w > ctas * wpc) {
+        wpc = w;
+        ctas = warps / w;
+      }
+    const size_t smem = size_t(wpc) * a.warp_bytes;
+    auto kern = gc <= 1 ? k_walk_rows<1> : (gc == 2 ? k_walk_rows<2> : k_walk_rows<4>);
+    RNNDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kern<<<unsigned(sm_count(c)) * ctas, 32 * wpc, smem, stream>>>(a);
+    ++c->launches;
+  }
+  RNNDG_CUDA(cudaGetLastError());
+}
+
+}  // namespace rnndg

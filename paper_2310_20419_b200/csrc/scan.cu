@@ -1400,6 +1400,14 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
     const char* e = std::getenv("RNNDG_BSP_STREAM");
     return e ? std::atoi(e) : 1;
   }();
+  bool used_side2 = false;
+  if (rowwalk_cap(c)) {
+    // short rows: lists of <= rowwalk_cap() entries are walked out of shared
+    // memory, one warp per list (rowwalk.cu), ahead of the short-list kernel
+    RNNDG_CUDA(cudaStreamWaitEvent(c->side2, c->ev_fork, 0));
+    launch_rowwalk(c, work, c->side2, spec);
+    used_side2 = true;
+  }
   if (bsp_rounds()) {
     a.skip_small = 1;
     if (bsp_stream) {
@@ -1414,7 +1422,7 @@ void launch_scan(rnndg_ctx* c, unsigned int* work) {
   if (c->trace) RNNDG_CUDA(cudaEventRecord(c->ev_scan[1], c->stream));
   RNNDG_CUDA(cudaEventRecord(c->ev_join, c->side));
   RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join, 0));
-  if (bsp_rounds() && bsp_stream) {
+  if ((bsp_rounds() && bsp_stream) || used_side2) {
     RNNDG_CUDA(cudaEventRecord(c->ev_join2, c->side2));
     RNNDG_CUDA(cudaStreamWaitEvent(c->stream, c->ev_join2, 0));
   }

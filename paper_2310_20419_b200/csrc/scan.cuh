@@ -35,6 +35,11 @@ void gram_trace(rnndg_ctx* c);
 int bsp_rounds();
 uint32_t bsp_max_len();
 void launch_bsp(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int spec, int l2pf);
+// shared-memory walk for short rows (rowwalk.cu): lists of at most
+// rowwalk_cap() entries (0 = off), queued by size class like the Gram walk's;
+// cursors at work[8 .. 12)
+uint32_t rowwalk_cap(rnndg_ctx* c);
+void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int spec);
 // provisional entries per push round (RNNDG_SPEC) and the hub-cluster size
 // (0 = one CTA per hub list); build.cu queues big hubs only when clustered
 int spec_mode();

@@ -3,7 +3,8 @@ knobs (read once per process, so tests/test_gpu_knobs.py starts this script
 per setting).  Two cases, each against the CPU oracle (oracle/rnnd_oracle.c,
 pinned to the reference):
 
-  passes  d = 67 (a d % 4 tail), imported lists of every size class -- Gram
+  passes  d = 67 (a d % 4 tail; RNNDG_CASE_D overrides it: d = 96 / 128 take
+          the shared-memory walk of rowwalk.cu), imported lists of every size class -- Gram
           tiles of 16/32/64/128 rows, short lists up to 384, hubs -- then
           update passes, a reverse phase and more passes; the whole graph and
           every EditCounts compared after each step
@@ -26,7 +27,7 @@ def case_passes() -> int:
     from oracle.oracle import CSR
     from paper_2310_20419_b200 import _lib, rnnd as R
 
-    n, d = 4000, 67
+    n, d = 4000, int(os.environ.get("RNNDG_CASE_D", "67"))
     data = oracle.synth_uniform(n, d, 5)
     rng = np.random.default_rng(3)
     sizes = [2, 9, 16, 17, 31, 32, 33, 63, 64, 65, 100, 127, 128, 129, 200, 383, 384, 385, 700,

@@ -37,6 +37,15 @@ KNOBS = [
     {"RNNDG_BSP": "6", "RNNDG_SPEC": "4"},
     {"RNNDG_BSP": "6", "RNNDG_SPEC": "2", "RNNDG_BSP_STREAM": "0"},
     {"RNNDG_BSP": "12", "RNNDG_BSP_STREAM": "2"},
+    # short rows (RNNDG_CASE_D sets the dimension of the `passes` case): the
+    # shared-memory walk (rowwalk.cu) on, capped, off, with other depths
+    {"RNNDG_CASE_D": "96"},
+    {"RNNDG_CASE_D": "128"},
+    {"RNNDG_CASE_D": "96", "RNNDG_ROWWALK": "32"},
+    {"RNNDG_CASE_D": "128", "RNNDG_ROWWALK": "0"},
+    {"RNNDG_CASE_D": "96", "RNNDG_SPEC": "4"},
+    {"RNNDG_CASE_D": "96", "RNNDG_SPEC": "2", "RNNDG_ROWWALK": "64"},
+    {"RNNDG_CASE_D": "144"},
 ]
 
 
