@@ -136,9 +136,13 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
                                                                           unsigned long long* __restrict__ ctr,
                                                     uint32_t ucap, uint32_t big_cap,
                                                     uint32_t ls_cap, uint32_t gcap,
+                                                    uint32_t gb0, uint32_t gb1, uint32_t gb2,
                                                     uint32_t* __restrict__ gq,
                                                     uint64_t* __restrict__ mat_b,
                                                     uint64_t* __restrict__ mat_e) {
+  constexpr uint32_t kQBuf = 16;
+  __shared__ uint32_t qbuf[8][4][kQBuf];  // per warp and size class (lane 0's)
+  uint32_t qn[4] = {0, 0, 0, 0};
   const uint32_t lane = lane_id();
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -167,10 +171,18 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
       nact += 1;
       maxlen = U > maxlen ? U : maxlen;
       flag = U > ucap ? 2 : (U > ls_cap ? 3 : 1);
-      if (U <= gcap) {  // Gram-filtered walk (gram.cu), queued by size class
-        const int gc = U <= 16 ? 0 : (U <= 32 ? 1 : (U <= 64 ? 2 : 3));
-        const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kGram0 + gc]), 1u);
-        gq[uint64_t(gc) * n + x] = uint32_t(u);
+      if (U <= gcap) {  // Gram-filtered walk (gram.cu) / shared-memory walk
+        // (rowwalk.cu), queued by size class: buffered per warp, one atomic per
+        // kQBuf lists (a million single-address atomics cost 0.5 ms per pass)
+        const int gc = U <= gb0 ? 0 : (U <= gb1 ? 1 : (U <= gb2 ? 2 : 3));
+        uint32_t* qb = qbuf[threadIdx.x >> 5][gc];
+        qb[qn[gc]++] = uint32_t(u);
+        if (qn[gc] == kQBuf) {
+          const uint32_t x =
+              atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kGram0 + gc]), uint32_t(kQBuf));
+          for (uint32_t i = 0; i < kQBuf; ++i) gq[uint64_t(gc) * n + x + i] = qb[i];
+          qn[gc] = 0;
+        }
         flag = 4;
       } else if (flag == 3) {  // long short list: queued ahead of the others, act_list[i]
         const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kLongShortCount]), 1u);
@@ -189,6 +201,12 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
     active[u] = flag;
   }
   if (lane == 0) {
+    for (int gc = 0; gc < 4; ++gc)
+      if (qn[gc]) {
+        const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kGram0 + gc]), qn[gc]);
+        for (uint32_t i = 0; i < qn[gc]; ++i)
+          gq[uint64_t(gc) * n + x + i] = qbuf[threadIdx.x >> 5][gc][i];
+      }
     if (skips) atomicAdd(&ctr[kFlagSkips], skips);
     if (aentries) atomicAdd(&ctr[kActiveEntries], aentries);
     if (nact) atomicAdd(&ctr[kActiveCount], nact);
@@ -1261,11 +1279,15 @@ void op_scan_phase(rnndg_ctx* c) {
   zero(c, c->bcnt.p, n + 1);
   zero(c, c->bcur.p, n);
   RNNDG_CUDA(cudaEventRecord(c->ev[0], c->stream));
+  // size classes of the per-class queues: the Gram walk's tiles, or the
+  // shared-memory walk's regions
+  uint32_t cls[4] = {16, 32, 64, 128};
+  if (!gram_cap() && rowwalk_cap(c)) rowwalk_classes(c, cls);
   if (n)
     RNNDG_LAUNCH(c, k_mark_active, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
                  big_hub_threshold(c), bsp_rounds() ? bsp_max_len() : long_short_threshold(),
-                 gram_cap() ? gram_cap() : rowwalk_cap(c), c->gram_q.p,
+                 gram_cap() ? gram_cap() : rowwalk_cap(c), cls[0], cls[1], cls[2], c->gram_q.p,
                  c->pending ? c->mat_b.ensure(n) : nullptr,
                  c->pending ? c->mat_e.ensure(2 * n) : nullptr);
   if (c->pending && n) {

@@ -36,6 +36,7 @@
 
 #include "common.cuh"
 #include "ctx.hpp"
+#include "quad.cuh"
 #include "scan.cuh"
 
 namespace rnndg {
@@ -105,21 +106,39 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
   const uint32_t count = uint32_t(*g.count);
   unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, evals = 0;
 
-  for (;;) {
+  // The next list's vertex, offset, length and keys are fetched while the
+  // current list's rows are still landing, so the chain of dependent global
+  // loads (queue -> off / cnt -> keys) is off the walk's critical path.
+  uint32_t u2 = 0, U2 = 0;
+  uint64_t base2 = 0, kk2[NP];
+  bool have2 = false;
+  auto fetch_next = [&]() {
     uint32_t it = 0;
     if (lane == 0) it = atomicAdd(g.cursor, 1u);
     it = __shfl_sync(0xffffffffu, it, 0);
-    if (it >= count) break;
-    const uint32_t u = g.queue[it];
-    const uint64_t base = g.off[u];
-    const uint32_t U = g.cnt[u];
+    have2 = it < count;
+    if (!have2) return;
+    u2 = g.queue[it];
+    base2 = g.off[u2];
+    U2 = g.cnt[u2];
+#pragma unroll
+    for (int k = 0; k < NP; ++k) {
+      const uint32_t p = 32u * k + lane;
+      kk2[k] = p < U2 ? g.keys[base2 + p] : 0ull;
+    }
+  };
+  fetch_next();
+  while (have2) {
+    const uint32_t u = u2;
+    const uint64_t base = base2;
+    const uint32_t U = U2;
     uint64_t* L = g.keys + base;
     uint64_t kk[NP];
     uint32_t M[NP], T[NP], F[NP];
 #pragma unroll
     for (int k = 0; k < NP; ++k) {
       const uint32_t p = 32u * k + lane;
-      kk[k] = p < U ? L[p] : 0ull;
+      kk[k] = kk2[k];
       M[k] = __ballot_sync(0xffffffffu, p < U);
       F[k] = __ballot_sync(0xffffffffu, p < U && key_fresh(kk[k]));
       T[k] = 0;
@@ -135,6 +154,8 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
         for (uint32_t c = lane; c < q4; c += 32) cp_async16(rows + r * rs + 4 * c, src + 4 * c);
       }
     }
+    fetch_next();  // in flight together with the row copies
+    bool pf_next = have2;
     cp_async_wait_all();
     __syncwarp();
     uint32_t nk = 0;
@@ -374,6 +395,14 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
           M[k] &= ~(km | gone_m[k]);
         }
       }
+      if (pf_next) {
+        // the next list's rows towards L2 (its keys have arrived by now)
+        pf_next = false;
+#pragma unroll
+        for (int k = 0; k < NP; ++k)
+          if (32u * k + lane < U2)
+            prefetch_row_l2(g.x + uint64_t(key_id(kk2[k])) * g.d, g.d * 4u);
+      }
     }
     if (lane == 0) {
       g.post_cnt[u] = nk;
@@ -420,6 +449,21 @@ uint32_t rowwalk_cap(rnndg_ctx* c) {
   return cap;
 }
 
+// Size classes: a warp's shared-memory region holds the class's longest list,
+// so finer classes mean more resident warps for the shorter lists.
+void rowwalk_classes(rnndg_ctx* c, uint32_t cls[4]) {
+  const uint32_t cap = rowwalk_cap(c);
+  if (cap >= 128) {
+    cls[0] = 32; cls[1] = 64; cls[2] = 96; cls[3] = 128;
+  } else if (cap >= 64) {
+    cls[0] = 16; cls[1] = 32; cls[2] = 48; cls[3] = 64;
+  } else if (cap >= 32) {
+    cls[0] = 12; cls[1] = 20; cls[2] = 26; cls[3] = 32;
+  } else {
+    cls[0] = 4; cls[1] = 8; cls[2] = 12; cls[3] = 16;
+  }
+}
+
 void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int spec) {
   const uint32_t cap = rowwalk_cap(c);
   if (!cap) return;
@@ -437,10 +481,20 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
   a.pend_key = c->pend_key.p;
   a.bcnt = c->partitioned ? nullptr : c->bcnt.p;
   a.ctr = c->counters.p;
-  a.D = spec < kMaxD ? spec : kMaxD;
-  const uint32_t class_rows[4] = {16, 32, 64, 128};
+  // provisional entries per speculative round (RNNDG_ROWWALK_D, 2 .. 4): here a
+  // step evaluates 32 pairs whether or not they are needed, so the depth is
+  // chosen to fill the steps, not to save pairs (the first pass over the
+  // random lists included, where the CTA kernels drop to 2)
+  static const int forced_d = [] {
+    const char* e = std::getenv("RNNDG_ROWWALK_D");
+    const int v = e ? std::atoi(e) : 0;
+    return v >= 2 && v <= kMaxD ? v : 0;
+  }();
+  (void)spec;
+  a.D = forced_d ? forced_d : 3;
+  uint32_t class_rows[4];
+  rowwalk_classes(c, class_rows);
   for (int gc = 3; gc >= 0; --gc) {  // the longest walks first
-    if (class_rows[gc] > cap) continue;
     a.queue = c->gram_q.p + uint64_t(gc) * n;
     a.count = c->counters.p + kGram0 + gc;
     a.cursor = work + 8 + gc;
@@ -459,7 +513,8 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
         ctas = warps / w;
       }
     const size_t smem = size_t(wpc) * a.warp_bytes;
-    auto kern = gc <= 1 ? k_walk_rows<1> : (gc == 2 ? k_walk_rows<2> : k_walk_rows<4>);
+    auto kern = class_rows[gc] <= 32 ? k_walk_rows<1>
+                                     : (class_rows[gc] <= 64 ? k_walk_rows<2> : k_walk_rows<4>);
     RNNDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<unsigned(sm_count(c)) * ctas, 32 * wpc, smem, stream>>>(a);
     ++c->launches;
