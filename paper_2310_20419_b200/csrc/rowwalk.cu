@@ -65,6 +65,7 @@ struct RowWalkArgs {
   unsigned long long* bcnt;
   unsigned long long* ctr;
   int D;
+  unsigned long long nz;      // (-0.0f, -0.0f), opaque to the compiler (dist_rows)
 };
 
 __device__ __forceinline__ uint32_t lt_mask(uint32_t lane) { return (1u << lane) - 1u; }
@@ -79,13 +80,35 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.wait_all;" ::: "memory");
 }
 
-// exact l2_sq of two shared-memory rows (metric.hpp:15-24 order; d % 4 == 0)
-__device__ __forceinline__ float dist_rows(const float* a, const float* b, uint32_t q4) {
-  const float4* a4 = reinterpret_cast<const float4*>(a);
-  const float4* b4 = reinterpret_cast<const float4*>(b);
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+// exact l2_sq of two shared-memory rows (metric.hpp:15-24 order; d % 4 == 0).
+// A lane owns all four chains, so one 128-bit read holds one element of each
+// and the three roundings of a step -- t = a - b, m = t * t, s = s + m -- run
+// as packed f32x2 instructions on the chain pairs (0, 1) and (2, 3): the same
+// IEEE round-to-nearest per element as the scalar FSUB / FMUL / FADD, at half
+// the FP32-pipe issue.  The square is fma(t, t, nz) with nz = (-0, -0) read
+// from the kernel arguments: adding -0 changes no value (a zero product
+// stays +0), and because ptxas cannot see the constant it cannot turn the
+// square and the following add into one fused multiply-add.
+__device__ __forceinline__ float dist_rows(const float* a, const float* b, uint32_t q4,
+                                           unsigned long long nz) {
+  const uint32_t pa = uint32_t(__cvta_generic_to_shared(a));
+  const uint32_t pb = uint32_t(__cvta_generic_to_shared(b));
+  unsigned long long s01 = 0ull, s23 = 0ull;  // (+0, +0)
 #pragma unroll 4
-  for (uint32_t c = 0; c < q4; ++c) l2_step4(a4[c], b4[c], s0, s1, s2, s3);
+  for (uint32_t c = 0; c < q4; ++c) {
+    unsigned long long a01, a23, b01, b23, t01, t23, m01, m23;
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a01), "=l"(a23) : "r"(pa + 16u * c));
+    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(b01), "=l"(b23) : "r"(pb + 16u * c));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t01) : "l"(a01), "l"(b01));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t23) : "l"(a23), "l"(b23));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(m01) : "l"(t01), "l"(nz));
+    asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(m23) : "l"(t23), "l"(nz));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s01) : "l"(s01), "l"(m01));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s23) : "l"(s23), "l"(m23));
+  }
+  float s0, s1, s2, s3;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(s0), "=f"(s1) : "l"(s01));
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(s2), "=f"(s3) : "l"(s23));
   return l2_finish(s0, s1, s2, s3);
 }
 
@@ -227,7 +250,7 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
         evals += lane == 0 ? ntask : 0u;
         for (uint32_t t = lane; t < ntask; t += 32) {
           const uint32_t i = t / nf, r = t - i * nf;
-          res[t] = dist_rows(rows + uint32_t(tpos[r]) * rs, rows + wp[i] * rs, q4);
+          res[t] = dist_rows(rows + uint32_t(tpos[r]) * rs, rows + wp[i] * rs, q4, g.nz);
         }
         __syncwarp();
         uint32_t reach = 0;
@@ -311,11 +334,13 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
           for (int i = 0; i < kMaxD; ++i)
             if (nm[k] >> i & 1u) tpos[idx[k][i]] = uint8_t(32u * k + lane);
         __syncwarp();
+        // (two pairs per lane per step, for more loads and chains in flight,
+        // measured no faster: the steps are not what the warps wait on)
         for (uint32_t t = lane; t < ntask; t += 32) {
           uint32_t i = 0;
 #pragma unroll
           for (int j = 1; j < kMaxD; ++j) i += t >= bases[j] ? 1u : 0u;
-          res[t] = dist_rows(rows + uint32_t(tpos[t]) * rs, rows + wp[i] * rs, q4);
+          res[t] = dist_rows(rows + uint32_t(tpos[t]) * rs, rows + wp[i] * rs, q4, g.nz);
         }
         __syncwarp();
         // the provisional entries publish their pairs; fates in list order,
@@ -481,6 +506,7 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
   a.pend_key = c->pend_key.p;
   a.bcnt = c->partitioned ? nullptr : c->bcnt.p;
   a.ctr = c->counters.p;
+  a.nz = 0x8000000080000000ull;
   // provisional entries per speculative round (RNNDG_ROWWALK_D, 2 .. 4): here a
   // step evaluates 32 pairs whether or not they are needed, so the depth is
   // chosen to fill the steps, not to save pairs (the first pass over the

@@ -20,11 +20,17 @@ import bench  # noqa: E402
 import datagen  # noqa: E402
 from oracle import oracle as O  # noqa: E402
 
+GPU_ONLY = "--gpu-only" in sys.argv  # re-measure the GPU legs, keep the recorded CPU legs
+sys.argv = [a for a in sys.argv if a != "--gpu-only"]
 names = sys.argv[1:] or ["C1-gmm128-20k", "C2-siftlike-1M", "C3-gistlike-1M", "C4-deeplike-1M",
                          "C5-deep10M"]
-out = {"date": datetime.datetime.utcnow().isoformat() + "Z", "cpu_model": bench.cpu_model(),
+out = {"date": datetime.datetime.now(datetime.timezone.utc).isoformat(), "cpu_model": bench.cpu_model(),
        "host_threads": max(len(os.sched_getaffinity(0)), 2), "configs": {}}
 path = os.path.join(ROOT, "gpurun_out", "side_by_side.json")
+prev = {}
+if GPU_ONLY:
+    prev = json.load(open(os.path.join(ROOT, "profiles", "r02_side_by_side_all_configs.json")))
+    out["cpu_legs_from"] = prev.get("date")
 for name in names:
     cfg = datagen.CONFIGS[name]
     rec = {}
@@ -38,6 +44,18 @@ for name in names:
                                             "e2e", "recall", "parity", "clocks", "gpu_launches")}
     except Exception as e:  # keep going: the CPU leg is still worth having
         rec["gpu"] = {"failed": str(e), "stderr": r.stderr[-500:]}
+    if GPU_ONLY:
+        rec["cpu_reference"] = prev["configs"][name]["cpu_reference"]
+        med, checks = rec["cpu_reference"]["seconds_median"], rec["cpu_reference"]["pair_checks"]
+        gb = rec["gpu"].get("build_seconds")
+        if gb:
+            rec["gpu_over_cpu_build_time"] = med / gb
+            rec["pair_checks_equal"] = rec["gpu"].get("pair_checks_per_build") == int(checks)
+        out["configs"][name] = rec
+        json.dump(out, open(path, "w"), indent=1)
+        print(name, json.dumps({"gpu_s": gb, "cpu_s": med,
+                                "checks_equal": rec.get("pair_checks_equal")}), flush=True)
+        continue
     data = bench.store_rows(cfg, cfg.n)
     runs = 1 if cfg.n > 2_000_000 else 3
     secs, checks = [], None
