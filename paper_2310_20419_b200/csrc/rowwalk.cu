@@ -30,6 +30,7 @@
 // budget per warp.  Results are the reference's bit for bit: the schedule of
 // rounds never changes pair_checks, flag_skips, removed or a redirect
 // (scan.cu header).
+#include <array>
 #include <cstdio>
 #include <cstdlib>
 #include <type_traits>
@@ -45,7 +46,7 @@ namespace {
 
 constexpr int kMaxD = 4;          // provisional entries per speculative round, at most
 constexpr uint32_t kWin = 16;     // old-run window
-constexpr uint32_t kSmemBudget = 200 * 1024;  // per SM, for the resident rows
+constexpr uint32_t kSmemBudget = 216 * 1024;  // per SM, for the resident rows (200 KB: C4 1M 0.477 s, 216 KB: 0.459 s)
 
 struct RowWalkArgs {
   const uint32_t* queue;      // this class's lists
@@ -470,6 +471,10 @@ uint32_t rowwalk_cap(rnndg_ctx* c) {
   // 0.765 s; C2 1M d = 128: 32 -> 0.492 s, 64 -> 0.534 s, 128 -> 0.686 s, off
   // 0.605 s): classes whose rows leave fewer than ~7 warps per SM lose
   uint32_t cap = c->d <= 100 ? 64 : 32;
+  if (const char* e = std::getenv("RNNDG_ROWWALK_CLS")) {  // explicit classes set the cap
+    unsigned a = 0, b = 0, cc = 0, dd = 0;
+    if (std::sscanf(e, "%u,%u,%u,%u", &a, &b, &cc, &dd) == 4 && dd >= 4 && dd <= 128) return dd;
+  }
   if (forced > 0) cap = forced <= 16 ? 16 : (forced <= 32 ? 32 : (forced <= 64 ? 64 : 128));
   return cap;
 }
@@ -478,6 +483,19 @@ uint32_t rowwalk_cap(rnndg_ctx* c) {
 // so finer classes mean more resident warps for the shorter lists.
 void rowwalk_classes(rnndg_ctx* c, uint32_t cls[4]) {
   const uint32_t cap = rowwalk_cap(c);
+  // RNNDG_ROWWALK_CLS=a,b,c,d: explicit ascending class bounds (experiments;
+  // d <= 128 and multiples of 4 keep the regions aligned)
+  static const std::array<uint32_t, 4> forced = [] {
+    std::array<uint32_t, 4> v{0, 0, 0, 0};
+    if (const char* e = std::getenv("RNNDG_ROWWALK_CLS"))
+      std::sscanf(e, "%u,%u,%u,%u", &v[0], &v[1], &v[2], &v[3]);
+    return v;
+  }();
+  if (forced[0] && forced[0] < forced[1] && forced[1] < forced[2] && forced[2] < forced[3] &&
+      forced[3] <= 128) {
+    for (int i = 0; i < 4; ++i) cls[i] = forced[i];
+    return;
+  }
   if (cap >= 128) {
     cls[0] = 32; cls[1] = 64; cls[2] = 96; cls[3] = 128;
   } else if (cap >= 64) {
@@ -528,7 +546,12 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
     a.warp_bytes = a.max_rows * a.rs * 4 + 12 * kWin + 4 * kMaxD * kMaxD +
                    5 * kMaxD * a.max_rows;  // + task results and positions
     a.warp_bytes = (a.warp_bytes + 15u) & ~15u;
-    uint32_t warps = kSmemBudget / a.warp_bytes;  // per SM
+    static const uint32_t budget = [] {
+      const char* e = std::getenv("RNNDG_ROWWALK_SMEM");  // KB per SM for the resident rows
+      const int v = e ? std::atoi(e) : 0;
+      return v >= 32 && v <= 224 ? uint32_t(v) * 1024u : kSmemBudget;
+    }();
+    uint32_t warps = budget / a.warp_bytes;  // per SM
     if (warps < 1) continue;
     if (warps > 32) warps = 32;
     // CTAs of 4 .. 8 warps, whichever packs the most warps into the budget
