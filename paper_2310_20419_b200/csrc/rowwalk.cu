@@ -113,11 +113,44 @@ __device__ __forceinline__ float dist_rows(const float* a, const float* b, uint3
   return l2_finish(s0, s1, s2, s3);
 }
 
-template <int NP>
-__global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
+// One list per CTA.  Warp 0 walks it; with NW > 1 the other warps are helpers
+// that share the two bulk steps -- the row copy and a round's evaluation --
+// between two block barriers.  The rows a list keeps resident bound how many
+// lists fit an SM, so for the larger size classes the helpers are lanes the
+// shared memory has already paid for.
+enum : uint32_t { kJobExit = 0, kJobCopy, kJobRun, kJobSpec };
+
+__device__ __forceinline__ void copy_rows(const RowWalkArgs& g, float* rows, const uint32_t* ids,
+                                          uint32_t U, uint32_t q4, uint32_t nt) {
+  for (uint32_t idx = threadIdx.x; idx < U * q4; idx += nt) {
+    const uint32_t r = idx / q4, c = idx - r * q4;
+    cp_async16(rows + r * g.rs + 4 * c, g.x + uint64_t(ids[r]) * g.d + 4 * c);
+  }
+}
+__device__ __forceinline__ void eval_run(const RowWalkArgs& g, const float* rows, const uint8_t* tpos,
+                                         const uint32_t* wp, float* res, uint32_t ntask, uint32_t nf,
+                                         uint32_t q4, uint32_t nt) {
+  for (uint32_t t = threadIdx.x; t < ntask; t += nt) {
+    const uint32_t i = t / nf, r = t - i * nf;
+    res[t] = dist_rows(rows + uint32_t(tpos[r]) * g.rs, rows + wp[i] * g.rs, q4, g.nz);
+  }
+}
+__device__ __forceinline__ void eval_spec(const RowWalkArgs& g, const float* rows,
+                                          const uint8_t* tpos, const uint32_t* wp, float* res,
+                                          uint32_t ntask, uint32_t b1, uint32_t b2, uint32_t b3,
+                                          uint32_t q4, uint32_t nt) {
+  for (uint32_t t = threadIdx.x; t < ntask; t += nt) {
+    const uint32_t i = (t >= b1 ? 1u : 0u) + (t >= b2 ? 1u : 0u) + (t >= b3 ? 1u : 0u);
+    res[t] = dist_rows(rows + uint32_t(tpos[t]) * g.rs, rows + wp[i] * g.rs, q4, g.nz);
+  }
+}
+
+template <int NP, int NW>
+__global__ void __launch_bounds__(32 * NW) k_walk_rows(RowWalkArgs g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr uint32_t NT = 32 * NW;
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;
-  unsigned char* wbase = smem_raw + size_t(wid) * g.warp_bytes;
+  unsigned char* wbase = smem_raw;
   float* rows = reinterpret_cast<float*>(wbase);
   unsigned char* tail = wbase + size_t(g.max_rows) * g.rs * 4;
   uint64_t* wk = reinterpret_cast<uint64_t*>(tail);            // window / provisional keys
@@ -126,7 +159,25 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
   const uint32_t tcap = kMaxD * g.max_rows;                     // tasks of a round, at most
   float* res = reinterpret_cast<float*>(tail + 12 * kWin + 4 * kMaxD * kMaxD);  // their distances
   uint8_t* tpos = reinterpret_cast<uint8_t*>(res + tcap);       // their candidates' positions
-  const uint32_t q4 = g.d >> 2, rs = g.rs;
+  uint32_t* job = reinterpret_cast<uint32_t*>(tpos + tcap);     // job, and its parameters
+  uint32_t* ids = reinterpret_cast<uint32_t*>(res);             // row ids during the copy
+  if (NW > 1 && wid > 0) {
+    const uint32_t q4h = g.d >> 2;
+    for (;;) {
+      __syncthreads();  // a job is posted
+      const uint32_t jb = job[0];
+      if (jb == kJobExit) return;
+      if (jb == kJobCopy) {
+        copy_rows(g, rows, ids, job[1], q4h, NT);
+        cp_async_wait_all();
+      } else if (jb == kJobRun)
+        eval_run(g, rows, tpos, wp, res, job[1], job[2], q4h, NT);
+      else
+        eval_spec(g, rows, tpos, wp, res, job[1], job[2], job[3], job[4], q4h, NT);
+      __syncthreads();  // its results are visible
+    }
+  }
+  const uint32_t q4 = g.d >> 2;
   const uint32_t count = uint32_t(*g.count);
   unsigned long long removed = 0, checks = 0, skips = 0, touched = 0, evals = 0;
 
@@ -170,18 +221,18 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
     // the list's rows -> shared memory, row r at rows + r * rs
     __syncwarp();  // the previous list's reads are done
 #pragma unroll
-    for (int k = 0; k < NP; ++k) {
-      const uint32_t r1 = U < 32u * (k + 1) ? U : 32u * (k + 1);
-      for (uint32_t r = 32u * k; r < r1; ++r) {
-        const uint32_t id = __shfl_sync(0xffffffffu, key_id(kk[k]), r & 31u);
-        const float* src = g.x + uint64_t(id) * g.d;
-        for (uint32_t c = lane; c < q4; c += 32) cp_async16(rows + r * rs + 4 * c, src + 4 * c);
-      }
+    for (int k = 0; k < NP; ++k)
+      if (32u * k + lane < U) ids[32u * k + lane] = key_id(kk[k]);
+    if (lane == 0) {
+      job[0] = kJobCopy;
+      job[1] = U;
     }
+    __syncthreads();
+    copy_rows(g, rows, ids, U, q4, NT);
     fetch_next();  // in flight together with the row copies
-    bool pf_next = have2;
     cp_async_wait_all();
-    __syncwarp();
+    __syncthreads();
+    bool pf_next = have2;
     uint32_t nk = 0;
 
     for (;;) {
@@ -249,11 +300,14 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
         __syncwarp();
         const uint32_t ntask = nf * wr;
         evals += lane == 0 ? ntask : 0u;
-        for (uint32_t t = lane; t < ntask; t += 32) {
-          const uint32_t i = t / nf, r = t - i * nf;
-          res[t] = dist_rows(rows + uint32_t(tpos[r]) * rs, rows + wp[i] * rs, q4, g.nz);
+        if (lane == 0) {
+          job[0] = kJobRun;
+          job[1] = ntask;
+          job[2] = nf;
         }
-        __syncwarp();
+        __syncthreads();
+        eval_run(g, rows, tpos, wp, res, ntask, nf, q4, NT);
+        __syncthreads();
         uint32_t reach = 0;
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
@@ -337,13 +391,16 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
         __syncwarp();
         // (two pairs per lane per step, for more loads and chains in flight,
         // measured no faster: the steps are not what the warps wait on)
-        for (uint32_t t = lane; t < ntask; t += 32) {
-          uint32_t i = 0;
-#pragma unroll
-          for (int j = 1; j < kMaxD; ++j) i += t >= bases[j] ? 1u : 0u;
-          res[t] = dist_rows(rows + uint32_t(tpos[t]) * rs, rows + wp[i] * rs, q4, g.nz);
+        if (lane == 0) {
+          job[0] = kJobSpec;
+          job[1] = ntask;
+          job[2] = bases[1];
+          job[3] = bases[2];
+          job[4] = bases[3];
         }
-        __syncwarp();
+        __syncthreads();
+        eval_spec(g, rows, tpos, wp, res, ntask, bases[1], bases[2], bases[3], q4, NT);
+        __syncthreads();
         // the provisional entries publish their pairs; fates in list order,
         // the same on every lane
 #pragma unroll
@@ -437,6 +494,10 @@ __global__ void __launch_bounds__(256) k_walk_rows(RowWalkArgs g) {
       for (int k = 0; k < NP; ++k) tc += __popc(T[k]);
       touched += tc;
     }
+  }
+  if (NW > 1) {
+    if (lane == 0) job[0] = kJobExit;
+    __syncthreads();
   }
   for (int o = 16; o; o >>= 1) {
     touched += __shfl_xor_sync(0xffffffffu, touched, o);
@@ -544,28 +605,32 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
     a.cursor = work + 8 + gc;
     a.max_rows = class_rows[gc];
     a.warp_bytes = a.max_rows * a.rs * 4 + 12 * kWin + 4 * kMaxD * kMaxD +
-                   5 * kMaxD * a.max_rows;  // + task results and positions
+                   5 * kMaxD * a.max_rows + 32;  // + task results, positions, the job words
     a.warp_bytes = (a.warp_bytes + 15u) & ~15u;
     static const uint32_t budget = [] {
       const char* e = std::getenv("RNNDG_ROWWALK_SMEM");  // KB per SM for the resident rows
       const int v = e ? std::atoi(e) : 0;
       return v >= 32 && v <= 224 ? uint32_t(v) * 1024u : kSmemBudget;
     }();
-    uint32_t warps = budget / a.warp_bytes;  // per SM
-    if (warps < 1) continue;
-    if (warps > 32) warps = 32;
-    // CTAs of 4 .. 8 warps, whichever packs the most warps into the budget
-    uint32_t wpc = warps < 8 ? warps : 8, ctas = warps / wpc;
-    for (uint32_t w = 4; w <= 8 && w <= warps; ++w)
-      if ((warps / w) * w > ctas * wpc) {
-        wpc = w;
-        ctas = warps / w;
-      }
-    const size_t smem = size_t(wpc) * a.warp_bytes;
-    auto kern = class_rows[gc] <= 32 ? k_walk_rows<1>
-                                     : (class_rows[gc] <= 64 ? k_walk_rows<2> : k_walk_rows<4>);
+    uint32_t lists = budget / a.warp_bytes;  // resident lists (CTAs) per SM
+    if (lists < 1) continue;
+    if (lists > 32) lists = 32;
+    // warps per list: helpers where the rows leave few lists per SM
+    // (RNNDG_ROWWALK_NW forces 1 | 2 | 4)
+    static const int forced_nw = [] {
+      const char* e = std::getenv("RNNDG_ROWWALK_NW");
+      const int v = e ? std::atoi(e) : 0;
+      return v == 1 || v == 2 || v == 4 ? v : 0;
+    }();
+    const int nw = forced_nw ? forced_nw : (lists >= 14 ? 1 : (lists >= 7 ? 2 : 4));
+    const size_t smem = a.warp_bytes;
+    const int np = class_rows[gc] <= 32 ? 1 : (class_rows[gc] <= 64 ? 2 : 4);
+    void (*kern)(RowWalkArgs) = nullptr;
+    if (np == 1) kern = nw == 1 ? k_walk_rows<1, 1> : (nw == 2 ? k_walk_rows<1, 2> : k_walk_rows<1, 4>);
+    if (np == 2) kern = nw == 1 ? k_walk_rows<2, 1> : (nw == 2 ? k_walk_rows<2, 2> : k_walk_rows<2, 4>);
+    if (np == 4) kern = nw == 1 ? k_walk_rows<4, 1> : (nw == 2 ? k_walk_rows<4, 2> : k_walk_rows<4, 4>);
     RNNDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kern<<<unsigned(sm_count(c)) * ctas, 32 * wpc, smem, stream>>>(a);
+    kern<<<unsigned(sm_count(c)) * lists, 32 * nw, smem, stream>>>(a);
     ++c->launches;
   }
   RNNDG_CUDA(cudaGetLastError());
