@@ -528,10 +528,10 @@ uint32_t rowwalk_cap(rnndg_ctx* c) {
   if (forced == 0 || gram_cap() || bsp_rounds()) return 0;
   if (c->d == 0 || c->d % 4 != 0 || c->d > 144) return 0;
   if (reinterpret_cast<uintptr_t>(c->x) % 16 != 0) return 0;
-  // measured (C4 1M d = 96: 64 -> 0.537 s, 32 -> 0.561 s, 128 -> 0.573 s, off
-  // 0.765 s; C2 1M d = 128: 32 -> 0.492 s, 64 -> 0.534 s, 128 -> 0.686 s, off
-  // 0.605 s): classes whose rows leave fewer than ~7 warps per SM lose
-  uint32_t cap = c->d <= 100 ? 64 : 32;
+  // measured with one list per CTA and classes 20 / 32 / 44 / 64 (C4 1M d = 96:
+  // 0.399 s; classes up to 80 / 96 / 128: 0.424 / 0.425 / 0.437 s; off 0.765 s.
+  // C2 1M d = 128: 0.421 s; up to 48 / 96: 0.422 / 0.458 s; off 0.605 s)
+  uint32_t cap = 64;
   if (const char* e = std::getenv("RNNDG_ROWWALK_CLS")) {  // explicit classes set the cap
     unsigned a = 0, b = 0, cc = 0, dd = 0;
     if (std::sscanf(e, "%u,%u,%u,%u", &a, &b, &cc, &dd) == 4 && dd >= 4 && dd <= 128) return dd;
@@ -560,7 +560,9 @@ void rowwalk_classes(rnndg_ctx* c, uint32_t cls[4]) {
   if (cap >= 128) {
     cls[0] = 32; cls[1] = 64; cls[2] = 96; cls[3] = 128;
   } else if (cap >= 64) {
-    cls[0] = 16; cls[1] = 32; cls[2] = 48; cls[3] = 64;
+    // 20 = the initial list length S of the paper's builds: most lists of an
+    // update phase's first passes
+    cls[0] = 20; cls[1] = 32; cls[2] = 44; cls[3] = 64;
   } else if (cap >= 32) {
     cls[0] = 12; cls[1] = 20; cls[2] = 26; cls[3] = 32;
   } else {
@@ -622,7 +624,11 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
       const int v = e ? std::atoi(e) : 0;
       return v == 1 || v == 2 || v == 4 ? v : 0;
     }();
-    const int nw = forced_nw ? forced_nw : (lists >= 14 ? 1 : (lists >= 7 ? 2 : 4));
+    // (helpers measured slower wherever tried -- C4 1M 0.407 s with one warp
+    // per list, 0.461 s with two: they double a list's registers, which then
+    // bound the resident lists instead of the rows -- so the default is 1)
+    const int nw = forced_nw ? forced_nw : 1;
+    (void)lists;
     const size_t smem = a.warp_bytes;
     const int np = class_rows[gc] <= 32 ? 1 : (class_rows[gc] <= 64 ? 2 : 4);
     void (*kern)(RowWalkArgs) = nullptr;
