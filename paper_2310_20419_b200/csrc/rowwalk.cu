@@ -146,7 +146,7 @@ __device__ __forceinline__ void eval_spec(const RowWalkArgs& g, const float* row
 }
 
 template <int NP, int NW>
-__global__ void __launch_bounds__(32 * NW) k_walk_rows(RowWalkArgs g) {
+__global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_walk_rows(RowWalkArgs g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr uint32_t NT = 32 * NW;
   const uint32_t lane = lane_id(), wid = threadIdx.x >> 5;

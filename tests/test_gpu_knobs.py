@@ -46,6 +46,12 @@ KNOBS = [
     {"RNNDG_CASE_D": "96", "RNNDG_SPEC": "4"},
     {"RNNDG_CASE_D": "96", "RNNDG_SPEC": "2", "RNNDG_ROWWALK": "64"},
     {"RNNDG_CASE_D": "144"},
+    # ... with helper warps per list, other size classes (up to 128 entries:
+    # the 4-word masks), a small shared-memory budget
+    {"RNNDG_CASE_D": "96", "RNNDG_ROWWALK_NW": "2"},
+    {"RNNDG_CASE_D": "128", "RNNDG_ROWWALK_NW": "4", "RNNDG_ROWWALK": "128"},
+    {"RNNDG_CASE_D": "96", "RNNDG_ROWWALK_CLS": "8,16,24,40", "RNNDG_ROWWALK_SMEM": "64"},
+    {"RNNDG_CASE_D": "32", "RNNDG_ROWWALK": "128", "RNNDG_ROWWALK_D": "4"},
 ]
 
 
