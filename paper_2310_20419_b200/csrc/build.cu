@@ -120,6 +120,12 @@ __global__ void k_fill_offsets(uint64_t n, uint32_t S, uint64_t* off, uint32_t* 
   if (u < n) cnt[u] = S;
 }
 
+// upper bounds of the size classes 0 .. kSizeClasses - 2 (the last class runs
+// up to the cap)
+struct ClassBounds {
+  uint32_t b[kSizeClasses - 1];
+};
+
 // ------------------------------------------------------------ mark active
 // active = the list holds a fresh entry (builder.cpp:53-56: otherwise every
 // pair is old/old and the scan only counts skips).  One warp per list
@@ -136,13 +142,13 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
                                                                           unsigned long long* __restrict__ ctr,
                                                     uint32_t ucap, uint32_t big_cap,
                                                     uint32_t ls_cap, uint32_t gcap,
-                                                    uint32_t gb0, uint32_t gb1, uint32_t gb2,
+                                                    ClassBounds gb,
                                                     uint32_t* __restrict__ gq,
                                                     uint64_t* __restrict__ mat_b,
                                                     uint64_t* __restrict__ mat_e) {
   constexpr uint32_t kQBuf = 16;
-  __shared__ uint32_t qbuf[8][4][kQBuf];  // per warp and size class (lane 0's)
-  uint32_t qn[4] = {0, 0, 0, 0};
+  __shared__ uint32_t qbuf[8][kSizeClasses][kQBuf];  // per warp and size class (lane 0's)
+  uint32_t qn[kSizeClasses] = {};
   const uint32_t lane = lane_id();
   const uint64_t warp = (uint64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const uint64_t nwarps = (uint64_t(gridDim.x) * blockDim.x) >> 5;
@@ -174,7 +180,9 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
       if (U <= gcap) {  // Gram-filtered walk (gram.cu) / shared-memory walk
         // (rowwalk.cu), queued by size class: buffered per warp, one atomic per
         // kQBuf lists (a million single-address atomics cost 0.5 ms per pass)
-        const int gc = U <= gb0 ? 0 : (U <= gb1 ? 1 : (U <= gb2 ? 2 : 3));
+        int gc = 0;
+#pragma unroll
+        for (int i = 0; i < kSizeClasses - 1; ++i) gc += U > gb.b[i] ? 1 : 0;
         uint32_t* qb = qbuf[threadIdx.x >> 5][gc];
         qb[qn[gc]++] = uint32_t(u);
         if (qn[gc] == kQBuf) {
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(256) k_mark_active(uint64_t n, const uint64_t*
     active[u] = flag;
   }
   if (lane == 0) {
-    for (int gc = 0; gc < 4; ++gc)
+    for (int gc = 0; gc < kSizeClasses; ++gc)
       if (qn[gc]) {
         const uint32_t x = atomicAdd(reinterpret_cast<unsigned int*>(&ctr[kGram0 + gc]), qn[gc]);
         for (uint32_t i = 0; i < qn[gc]; ++i)
@@ -933,7 +941,7 @@ void ensure_scratch(rnndg_ctx* c) {
   c->label.ensure(2 * n);
   c->okey.ensure(2 * n);
   c->act_small.ensure(n);
-  c->gram_q.ensure(4 * n + 1);
+  c->gram_q.ensure(kSizeClasses * n + 1);
   c->key_s.ensure(span);
   c->pend_src.ensure(span);
   c->pend_key.ensure(span);
@@ -1281,13 +1289,15 @@ void op_scan_phase(rnndg_ctx* c) {
   RNNDG_CUDA(cudaEventRecord(c->ev[0], c->stream));
   // size classes of the per-class queues: the Gram walk's tiles, or the
   // shared-memory walk's regions
-  uint32_t cls[4] = {16, 32, 64, 128};
+  uint32_t cls[kSizeClasses] = {16, 32, 64, 128, 128, 128, 128, 128};
   if (!gram_cap() && rowwalk_cap(c)) rowwalk_classes(c, cls);
+  ClassBounds gb;
+  for (int i = 0; i < kSizeClasses - 1; ++i) gb.b[i] = cls[i];
   if (n)
     RNNDG_LAUNCH(c, k_mark_active, warp_grid(c, n), kBlock, 0, n, c->off.p, c->cnt.p, c->key.p,
                  c->active.p, c->act_list.p, c->post_cnt.p, ctr, hub_threshold(),
                  big_hub_threshold(c), bsp_rounds() ? bsp_max_len() : long_short_threshold(),
-                 gram_cap() ? gram_cap() : rowwalk_cap(c), cls[0], cls[1], cls[2], c->gram_q.p,
+                 gram_cap() ? gram_cap() : rowwalk_cap(c), gb, c->gram_q.p,
                  c->pending ? c->mat_b.ensure(n) : nullptr,
                  c->pending ? c->mat_e.ensure(2 * n) : nullptr);
   if (c->pending && n) {

@@ -63,6 +63,8 @@ struct DevBuf {
   }
 };
 
+constexpr int kSizeClasses = 8;  // per-class list queues (k_mark_active)
+
 // Device-side counters of one pass (reduced with atomics).
 enum Counter : int {
   kRemoved = 0,
@@ -82,6 +84,10 @@ enum Counter : int {
   kGram1,      //   walk (gram.cu), one counter per size class
   kGram2,
   kGram3,
+  kClass4,     // ... and four more size classes for the shared-memory walk
+  kClass5,     //   (rowwalk.cu queues lists in up to kSizeClasses classes)
+  kClass6,
+  kClass7,
   kGramAmb,    // Gram-filter comparisons inside the error band (decided exactly)
   kGramExact,  // exact distances evaluated by the Gram-filtered walk
   kMatCount,   // lists queued for resolve_pending (build.cu)

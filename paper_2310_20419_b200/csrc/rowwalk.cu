@@ -533,8 +533,13 @@ uint32_t rowwalk_cap(rnndg_ctx* c) {
   // C2 1M d = 128: 0.421 s; up to 48 / 96: 0.422 / 0.458 s; off 0.605 s)
   uint32_t cap = 64;
   if (const char* e = std::getenv("RNNDG_ROWWALK_CLS")) {  // explicit classes set the cap
-    unsigned a = 0, b = 0, cc = 0, dd = 0;
-    if (std::sscanf(e, "%u,%u,%u,%u", &a, &b, &cc, &dd) == 4 && dd >= 4 && dd <= 128) return dd;
+    unsigned last = 0;
+    for (const char* p = e; *p;) {
+      last = unsigned(std::strtoul(p, nullptr, 10));
+      while (*p && *p != ',') ++p;
+      if (*p == ',') ++p;
+    }
+    if (last >= 4 && last <= 128) return last;
   }
   if (forced > 0) cap = forced <= 16 ? 16 : (forced <= 32 ? 32 : (forced <= 64 ? 64 : 128));
   return cap;
@@ -542,32 +547,43 @@ uint32_t rowwalk_cap(rnndg_ctx* c) {
 
 // Size classes: a warp's shared-memory region holds the class's longest list,
 // so finer classes mean more resident warps for the shorter lists.
-void rowwalk_classes(rnndg_ctx* c, uint32_t cls[4]) {
+void rowwalk_classes(rnndg_ctx* c, uint32_t cls[kSizeClasses]) {
   const uint32_t cap = rowwalk_cap(c);
-  // RNNDG_ROWWALK_CLS=a,b,c,d: explicit ascending class bounds (experiments;
-  // d <= 128 and multiples of 4 keep the regions aligned)
-  static const std::array<uint32_t, 4> forced = [] {
-    std::array<uint32_t, 4> v{0, 0, 0, 0};
-    if (const char* e = std::getenv("RNNDG_ROWWALK_CLS"))
-      std::sscanf(e, "%u,%u,%u,%u", &v[0], &v[1], &v[2], &v[3]);
+  // RNNDG_ROWWALK_CLS=a,b,...: explicit ascending class bounds (up to 8;
+  // experiments); the last one is the cap
+  static const std::array<uint32_t, kSizeClasses> forced = [] {
+    std::array<uint32_t, kSizeClasses> v{};
+    if (const char* e = std::getenv("RNNDG_ROWWALK_CLS")) {
+      int n = 0;
+      for (const char* p = e; *p && n < kSizeClasses;) {
+        v[n++] = uint32_t(std::strtoul(p, nullptr, 10));
+        while (*p && *p != ',') ++p;
+        if (*p == ',') ++p;
+      }
+      for (int i = n; i < kSizeClasses; ++i) v[i] = n ? v[n - 1] : 0;
+    }
     return v;
   }();
-  if (forced[0] && forced[0] < forced[1] && forced[1] < forced[2] && forced[2] < forced[3] &&
-      forced[3] <= 128) {
-    for (int i = 0; i < 4; ++i) cls[i] = forced[i];
+  bool ok = forced[0] > 0 && forced[kSizeClasses - 1] <= 128;
+  for (int i = 1; i < kSizeClasses; ++i) ok = ok && forced[i] >= forced[i - 1];
+  if (ok) {
+    for (int i = 0; i < kSizeClasses; ++i) cls[i] = forced[i];
     return;
   }
-  if (cap >= 128) {
-    cls[0] = 32; cls[1] = 64; cls[2] = 96; cls[3] = 128;
-  } else if (cap >= 64) {
-    // 20 = the initial list length S of the paper's builds: most lists of an
-    // update phase's first passes
-    cls[0] = 20; cls[1] = 32; cls[2] = 44; cls[3] = 64;
-  } else if (cap >= 32) {
-    cls[0] = 12; cls[1] = 20; cls[2] = 26; cls[3] = 32;
-  } else {
-    cls[0] = 4; cls[1] = 8; cls[2] = 12; cls[3] = 16;
-  }
+  // a region holds its class's longest list, so finer classes mean more
+  // resident lists; 20 = the initial list length S of the paper's builds
+  // (most lists of an update phase's first passes)
+  // (small stores are launch-bound: four classes -- duplicates are skipped --
+  // keep C1 20k at 0.019 s where eight cost 0.022 s; at 1M / 10M rows eight
+  // classes gain 1.5-3%: C4 1M 0.396 -> 0.389 s, C5 10M 7.15 -> 6.95 s)
+  static const uint32_t k64s[kSizeClasses] = {20, 20, 32, 32, 44, 44, 64, 64};
+  static const uint32_t k64[kSizeClasses] = {12, 16, 20, 26, 32, 40, 50, 64};
+  static const uint32_t k128[kSizeClasses] = {16, 20, 32, 44, 64, 80, 100, 128};
+  static const uint32_t k32[kSizeClasses] = {8, 12, 16, 20, 24, 28, 32, 32};
+  static const uint32_t k16[kSizeClasses] = {4, 6, 8, 10, 12, 14, 16, 16};
+  const uint32_t* t = cap >= 128 ? k128 : (cap >= 64 ? k64 : (cap >= 32 ? k32 : k16));
+  if (cap == 64 && c->nv < (1u << 18)) t = k64s;
+  for (int i = 0; i < kSizeClasses; ++i) cls[i] = t[i];
 }
 
 void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int spec) {
@@ -599,9 +615,10 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
   }();
   (void)spec;
   a.D = forced_d ? forced_d : 3;
-  uint32_t class_rows[4];
+  uint32_t class_rows[kSizeClasses];
   rowwalk_classes(c, class_rows);
-  for (int gc = 3; gc >= 0; --gc) {  // the longest walks first
+  for (int gc = kSizeClasses - 1; gc >= 0; --gc) {  // the longest walks first
+    if (gc > 0 && class_rows[gc] == class_rows[gc - 1]) continue;  // an empty (duplicate) class
     a.queue = c->gram_q.p + uint64_t(gc) * n;
     a.count = c->counters.p + kGram0 + gc;
     a.cursor = work + 8 + gc;

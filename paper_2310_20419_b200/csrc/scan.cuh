@@ -39,7 +39,7 @@ void launch_bsp(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int spec,
 // rowwalk_cap() entries (0 = off), queued by size class like the Gram walk's;
 // cursors at work[8 .. 12)
 uint32_t rowwalk_cap(rnndg_ctx* c);
-void rowwalk_classes(rnndg_ctx* c, uint32_t cls[4]);  // upper bounds of its 4 size classes
+void rowwalk_classes(rnndg_ctx* c, uint32_t cls[8]);  // upper bounds of its 8 size classes (ctx.hpp kSizeClasses)
 void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int spec);
 // provisional entries per push round (RNNDG_SPEC) and the hub-cluster size
 // (0 = one CTA per hub list); build.cu queues big hubs only when clustered
