@@ -145,7 +145,7 @@ __device__ __forceinline__ void eval_spec(const RowWalkArgs& g, const float* row
   }
 }
 
-template <int NP, int NW>
+template <int NP, int NW, int MD>
 __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_walk_rows(RowWalkArgs g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   constexpr uint32_t NT = 32 * NW;
@@ -355,8 +355,8 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_
         // where a flag is fresh; the provisional entries w_2 .. w_De are
         // candidates too (their pairs decide the fates).
         __syncwarp();
-        uint32_t nm[NP], lim[NP], idx[NP][kMaxD];
-        uint32_t bases[kMaxD + 1];
+        uint32_t nm[NP], lim[NP], idx[NP][MD];
+        uint32_t bases[kMaxD + 1] = {};
         bases[0] = 0;
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
@@ -366,12 +366,12 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_
           lim[k] = al ? (ai < De ? ai : De) : 0u;
           uint32_t m = 0;
 #pragma unroll
-          for (int i = 0; i < kMaxD; ++i)
+          for (int i = 0; i < MD; ++i)
             if (uint32_t(i) < lim[k] && (key_fresh(wk[i]) || vf)) m |= 1u << i;
           nm[k] = m;
         }
 #pragma unroll
-        for (int i = 0; i < kMaxD; ++i) {
+        for (int i = 0; i < MD; ++i) {
           uint32_t c = 0;
 #pragma unroll
           for (int k = 0; k < NP; ++k) {
@@ -381,12 +381,14 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_
           }
           bases[i + 1] = bases[i] + c;
         }
-        const uint32_t ntask = bases[kMaxD];
+        const uint32_t ntask = bases[MD];
+#pragma unroll
+        for (int i = MD + 1; i <= kMaxD; ++i) bases[i] = ntask;
         evals += lane == 0 ? ntask : 0u;
 #pragma unroll
         for (int k = 0; k < NP; ++k)
 #pragma unroll
-          for (int i = 0; i < kMaxD; ++i)
+          for (int i = 0; i < MD; ++i)
             if (nm[k] >> i & 1u) tpos[idx[k][i]] = uint8_t(32u * k + lane);
         __syncwarp();
         // (two pairs per lane per step, for more loads and chains in flight,
@@ -408,7 +410,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_
           const uint32_t j = arank[k];
           if ((M[k] >> lane & 1u) && j >= 1 && j < De)
 #pragma unroll
-            for (int i = 0; i < kMaxD; ++i)
+            for (int i = 0; i < MD; ++i)
               if (nm[k] >> i & 1u) fd[j * kMaxD + i] = res[idx[k][i]];
         }
         __syncwarp();
@@ -429,7 +431,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_
           const uint64_t vk = kk[k];
           const uint32_t q = 32u * k + lane;
 #pragma unroll
-          for (int i = 0; i < kMaxD; ++i) {
+          for (int i = 0; i < MD; ++i) {
             if (uint32_t(i) >= lim[k] || gone) continue;
             if (!(kept >> i & 1u)) continue;  // not in the reference's kept list
             if (!(nm[k] >> i & 1u)) {
@@ -458,7 +460,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_
         {
           uint32_t n2 = nk;
 #pragma unroll
-          for (int i = 0; i < kMaxD; ++i)
+          for (int i = 0; i < MD; ++i)
             if (uint32_t(i) < De && (kept >> i & 1u)) {
               if (lane == 0) L[n2] = wk[i] & ~1ull;
               ++n2;
@@ -467,13 +469,11 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_
         }
 #pragma unroll
         for (int k = 0; k < NP; ++k) {
-          uint32_t km = 0, tm = 0;
-#pragma unroll
-          for (int i = 0; i < kMaxD; ++i)
-            if (uint32_t(i) < De && (wp[i] >> 5) == uint32_t(k)) {
-              if (kept >> i & 1u) km |= 1u << (wp[i] & 31u);
-              if (wtouch >> i & 1u) tm |= 1u << (wp[i] & 31u);
-            }
+          // a provisional entry leaves the alive set when kept, and is touched
+          // when some candidate had a counted check with it
+          const bool prov = (M[k] >> lane & 1u) && arank[k] < De;
+          const uint32_t km = __ballot_sync(0xffffffffu, prov && (kept >> arank[k] & 1u));
+          const uint32_t tm = __ballot_sync(0xffffffffu, prov && (wtouch >> arank[k] & 1u));
           T[k] |= touch_m[k] | tm;
           M[k] &= ~(km | gone_m[k]);
         }
@@ -649,9 +649,15 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
     const size_t smem = a.warp_bytes;
     const int np = class_rows[gc] <= 32 ? 1 : (class_rows[gc] <= 64 ? 2 : 4);
     void (*kern)(RowWalkArgs) = nullptr;
-    if (np == 1) kern = nw == 1 ? k_walk_rows<1, 1> : (nw == 2 ? k_walk_rows<1, 2> : k_walk_rows<1, 4>);
-    if (np == 2) kern = nw == 1 ? k_walk_rows<2, 1> : (nw == 2 ? k_walk_rows<2, 2> : k_walk_rows<2, 4>);
-    if (np == 4) kern = nw == 1 ? k_walk_rows<4, 1> : (nw == 2 ? k_walk_rows<4, 2> : k_walk_rows<4, 4>);
+    if (a.D <= 3) {  // (the common depth: one iteration less in every unrolled loop over w)
+      if (np == 1) kern = nw == 1 ? k_walk_rows<1, 1, 3> : (nw == 2 ? k_walk_rows<1, 2, 3> : k_walk_rows<1, 4, 3>);
+      if (np == 2) kern = nw == 1 ? k_walk_rows<2, 1, 3> : (nw == 2 ? k_walk_rows<2, 2, 3> : k_walk_rows<2, 4, 3>);
+      if (np == 4) kern = nw == 1 ? k_walk_rows<4, 1, 3> : (nw == 2 ? k_walk_rows<4, 2, 3> : k_walk_rows<4, 4, 3>);
+    } else {
+      if (np == 1) kern = nw == 1 ? k_walk_rows<1, 1, 4> : (nw == 2 ? k_walk_rows<1, 2, 4> : k_walk_rows<1, 4, 4>);
+      if (np == 2) kern = nw == 1 ? k_walk_rows<2, 1, 4> : (nw == 2 ? k_walk_rows<2, 2, 4> : k_walk_rows<2, 4, 4>);
+      if (np == 4) kern = nw == 1 ? k_walk_rows<4, 1, 4> : (nw == 2 ? k_walk_rows<4, 2, 4> : k_walk_rows<4, 4, 4>);
+    }
     RNNDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     kern<<<unsigned(sm_count(c)) * lists, 32 * nw, smem, stream>>>(a);
     ++c->launches;
