@@ -92,16 +92,18 @@ __device__ __forceinline__ void cp_async_wait_all() {
 // square and the following add into one fused multiply-add.
 __device__ __forceinline__ float dist_rows(const float* a, const float* b, uint32_t q4,
                                            unsigned long long nz) {
-  const uint32_t pa = uint32_t(__cvta_generic_to_shared(a));
-  const uint32_t pb = uint32_t(__cvta_generic_to_shared(b));
+  // (plain 128-bit loads, not inline asm: unrolled, they take immediate
+  // offsets from one address register per row -- with asm loads a third of
+  // the loop's instructions were address arithmetic)
+  const ulonglong2* a2 = reinterpret_cast<const ulonglong2*>(a);
+  const ulonglong2* b2 = reinterpret_cast<const ulonglong2*>(b);
   unsigned long long s01 = 0ull, s23 = 0ull;  // (+0, +0)
-#pragma unroll 4
+#pragma unroll 8
   for (uint32_t c = 0; c < q4; ++c) {
-    unsigned long long a01, a23, b01, b23, t01, t23, m01, m23;
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(a01), "=l"(a23) : "r"(pa + 16u * c));
-    asm volatile("ld.shared.v2.u64 {%0, %1}, [%2];" : "=l"(b01), "=l"(b23) : "r"(pb + 16u * c));
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t01) : "l"(a01), "l"(b01));
-    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t23) : "l"(a23), "l"(b23));
+    const ulonglong2 av = a2[c], bv = b2[c];
+    unsigned long long t01, t23, m01, m23;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t01) : "l"(av.x), "l"(bv.x));
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(t23) : "l"(av.y), "l"(bv.y));
     asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(m01) : "l"(t01), "l"(nz));
     asm("fma.rn.f32x2 %0, %1, %1, %2;" : "=l"(m23) : "l"(t23), "l"(nz));
     asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s01) : "l"(s01), "l"(m01));
@@ -122,9 +124,17 @@ enum : uint32_t { kJobExit = 0, kJobCopy, kJobRun, kJobSpec };
 
 __device__ __forceinline__ void copy_rows(const RowWalkArgs& g, float* rows, const uint32_t* ids,
                                           uint32_t U, uint32_t q4, uint32_t nt) {
-  for (uint32_t idx = threadIdx.x; idx < U * q4; idx += nt) {
-    const uint32_t r = idx / q4, c = idx - r * q4;
+  // chunk idx = r * q4 + c, stepped by nt without a division per chunk
+  const uint32_t dr = nt / q4, dc = nt - dr * q4;
+  uint32_t r = threadIdx.x / q4, c = threadIdx.x - r * q4;
+  while (r < U) {
     cp_async16(rows + r * g.rs + 4 * c, g.x + uint64_t(ids[r]) * g.d + 4 * c);
+    r += dr;
+    c += dc;
+    if (c >= q4) {
+      c -= q4;
+      ++r;
+    }
   }
 }
 __device__ __forceinline__ void eval_run(const RowWalkArgs& g, const float* rows, const uint8_t* tpos,
