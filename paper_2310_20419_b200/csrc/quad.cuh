@@ -37,6 +37,23 @@ __device__ __forceinline__ void ld256w(const float* p, float (&r)[8]) {
                : "l"(p));
 }
 
+// the same loads at a compile-time byte offset from the pointer (the address
+// operand takes [reg + imm], so an unrolled loop bumps one register per row
+// instead of computing an address per load)
+template <bool kNA, int kOff>
+__device__ __forceinline__ void ld256o(const float* p, float (&r)[8]) {
+  if (kNA)
+    asm volatile("ld.global.nc.L1::no_allocate.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8+%9];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                   "=f"(r[6]), "=f"(r[7])
+                 : "l"(p), "n"(kOff));
+  else
+    asm volatile("ld.global.nc.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8+%9];"
+                 : "=f"(r[0]), "=f"(r[1]), "=f"(r[2]), "=f"(r[3]), "=f"(r[4]), "=f"(r[5]),
+                   "=f"(r[6]), "=f"(r[7])
+                 : "l"(p), "n"(kOff));
+}
+
 __device__ __forceinline__ void prefetch_row_l2(const float* p, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
 }
@@ -67,13 +84,15 @@ __device__ __forceinline__ float quad_l2(const float* __restrict__ a, const floa
     ld256w(pb, b0);
     ld256<kNA>(pa + 32, a1);
     ld256w(pb + 32, b1);
-    for (blk = 2; blk + 1 < nblk; blk += 2) {
+    const float* qa = pa + 64;
+    const float* qb = pb + 64;
+    for (blk = 2; blk + 1 < nblk; blk += 2, qa += 64, qb += 64) {
       chain_step(a0, b0, s);
-      ld256<kNA>(pa + 32 * blk, a0);
-      ld256w(pb + 32 * blk, b0);
+      ld256o<kNA, 0>(qa, a0);
+      ld256o<false, 0>(qb, b0);
       chain_step(a1, b1, s);
-      ld256<kNA>(pa + 32 * (blk + 1), a1);
-      ld256w(pb + 32 * (blk + 1), b1);
+      ld256o<kNA, 128>(qa, a1);
+      ld256o<false, 128>(qb, b1);
     }
     chain_step(a0, b0, s);
     chain_step(a1, b1, s);
