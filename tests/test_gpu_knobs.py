@@ -1,8 +1,10 @@
 """Every schedule knob that is kept gives the oracle's graph
 and counters bit for bit: the Gram-filtered walk on / off / capped, the
 short-list kernel's provisional depth, old-run rounds, list orders, the CUB
-sort, the one-CTA-per-hub widths.  Each setting runs tests/knob_case.py in
-its own process (the knobs are read once per process)."""
+sort, the one-CTA-per-hub widths, the round-synchronous walk (bsp.cu), and --
+on short rows -- the shared-memory walk (rowwalk.cu) on / capped / off, with
+helper warps, other size classes and depths.  Each setting runs
+tests/knob_case.py in its own process (the knobs are read once per process)."""
 import os
 import subprocess
 import sys
