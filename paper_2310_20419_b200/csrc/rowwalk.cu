@@ -286,10 +286,7 @@ __global__ void __launch_bounds__(32 * NW, NW == 1 ? (NP == 1 ? 24 : 12) : 1) k_
         }
       }
       uint32_t wr = run < kWin ? run : kWin;
-      {
-        const uint32_t cap = tcap / (nf ? nf : 1u);  // window x fresh candidates must fit
-        if (wr > cap) wr = cap;
-      }
+      if (wr * nf > tcap) wr = tcap / nf;  // window x fresh candidates must fit (rarely binds)
       const bool run_round = wr >= 2;
       const uint32_t De = run_round ? wr : (na < uint32_t(g.D) ? na : uint32_t(g.D));
       __syncwarp();
@@ -668,7 +665,18 @@ void launch_rowwalk(rnndg_ctx* c, unsigned int* work, cudaStream_t stream, int s
       if (np == 2) kern = nw == 1 ? k_walk_rows<2, 1, 4> : (nw == 2 ? k_walk_rows<2, 2, 4> : k_walk_rows<2, 4, 4>);
       if (np == 4) kern = nw == 1 ? k_walk_rows<4, 1, 4> : (nw == 2 ? k_walk_rows<4, 2, 4> : k_walk_rows<4, 4, 4>);
     }
-    RNNDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // the attribute is per function, not per launch: several host threads
+    // (csrc/multi.cu drives one context each) launch the same instantiation
+    // with different class sizes, so it is always set to the device maximum
+    // -- a per-class value set by one thread could be lowered by another
+    // between that thread's set and its launch
+    static thread_local int optin_dev = -1, optin = 0;
+    if (optin_dev != c->device) {
+      RNNDG_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, c->device));
+      optin_dev = c->device;
+    }
+    if (smem > size_t(optin)) continue;
+    RNNDG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
     kern<<<unsigned(sm_count(c)) * lists, 32 * nw, smem, stream>>>(a);
     ++c->launches;
   }
